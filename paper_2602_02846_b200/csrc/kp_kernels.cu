@@ -1,0 +1,670 @@
+// kp_kernels.cu — the three per-iteration kernels of the B200 Kino-PAX+ planner
+// plus reset/start/debug/trajectory helpers.
+//
+// One iteration (Alg. 1 lines 6-9) = three launches on one
+// stream, captured M iterations at a time into a CUDA graph:
+//
+//   k_propagate<MODEL>   Alg. 2.  One thread per V_U slot
+//                        (frontier position x branch).  Philox/SplitMix draw,
+//                        RK4 rollout streamed in registers with per-sample
+//                        validity against obstacles staged in shared memory,
+//                        path length, region, atomicMin on the encoded region
+//                        cost.  Admitted lanes write their slot record; a warp
+//                        ballot writes the admit / goal bitmask word.
+//   k_select_reduce      Alg. 3 + the commit test of Alg. 4.
+//                        Element space = [live nodes, padded to 32] ++ [slots].
+//                        Live nodes: prune rules in SPEC.md:434-437 priority
+//                        order; slots: commit iff admitted and acc bits ==
+//                        region minimum.  Per-tile counts (keep, active,
+//                        commit); the last block scans the tile counts.
+//   k_select_scatter     Re-derives each element's flags, block scan + tile
+//                        prefix -> positions.  Survivors go to the next live /
+//                        frontier lists in id order; committed slots get node
+//                        ids count + rank in slot order (so ids equal the
+//                        reference's workers=1 serial order), their records
+//                        are written to the SoA node store, goal leaves do a
+//                        64-bit atomicMin on (cost bits << 32 | id).  The last
+//                        block closes the iteration: counts, stats, best /
+//                        timeline / TTFS from %globaltimer, termination.
+//
+// No kernel waits on another block: cross-block results flow through the
+// "last block" ticket pattern (threadfence + atomic counter), never a spin.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kp_math.cuh"
+#include "kp_types.h"
+
+namespace kp {
+
+KP_DEV unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Stage obstacles into shared memory (boxes then spheres).
+KP_DEV void stage_obstacles(const KpProblem& P, const KpBuffers& B, float* sbox, float* ssph) {
+    for (int i = threadIdx.x; i < P.n_box * 6; i += blockDim.x) sbox[i] = B.boxes[i];
+    for (int i = threadIdx.x; i < P.n_sph * 4; i += blockDim.x) ssph[i] = B.spheres[i];
+    __syncthreads();
+}
+
+template <int MODEL>
+__global__ void __launch_bounds__(256) k_propagate(KpProblem P, KpBuffers B) {
+    constexpr int N = Model<MODEL>::N;
+    constexpr int M = Model<MODEL>::M;
+    extern __shared__ float smem[];
+    float* sbox = smem;
+    float* ssph = smem + 6 * P.n_box;
+    __shared__ unsigned long long s_cnt[4];
+    KpCtl* ctl = B.ctl;
+    if (ctl->done) return;
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    stage_obstacles(P, B, sbox, ssph);
+    const uint32_t n_items = ctl->n_items;
+    const uint32_t it = ctl->iter;
+    const unsigned long long seed = ctl->seed;
+    const uint32_t* __restrict__ va = B.va[it & 1];
+    const uint32_t padded = (n_items + 31u) & ~31u;
+    const uint32_t cap = P.capacity, S = P.max_slots;
+    const uint32_t lam = static_cast<uint32_t>(P.lambda);
+    uint32_t n_valid = 0, n_adm = 0, n_steps = 0, n_pts = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < padded; i += gridDim.x * blockDim.x) {
+        bool adm = false, goal = false;
+        if (i < n_items) {
+            const uint32_t f = i / lam;
+            const uint32_t br = i - f * lam;
+            const uint32_t node = va[f];
+            float x[N], u[M], dt;
+#pragma unroll
+            for (int d = 0; d < N; ++d) x[d] = B.state[static_cast<size_t>(d) * cap + node];
+            const float acc_p = __uint_as_float(B.acc[node]);
+            ItemOut o;
+            const int rc = propagate_item<MODEL>(P, sbox, ssph, x, acc_p, seed, it, node, br, u, dt, o);
+            n_steps += o.steps;
+            n_pts += o.points;
+            if (rc == 0) {
+                ++n_valid;
+                const uint32_t bits = __float_as_uint(o.acc);
+                const uint32_t old = atomicMin(B.rc + o.region, bits);
+                adm = bits <= old;  // Improved or Equal
+                if (adm) {
+                    ++n_adm;
+                    goal = o.goal;
+#pragma unroll
+                    for (int d = 0; d < N; ++d) B.vu_state[static_cast<size_t>(d) * S + i] = x[d];
+#pragma unroll
+                    for (int d = 0; d < M; ++d) B.vu_ctrl[static_cast<size_t>(d) * S + i] = u[d];
+                    B.vu_dt[i] = dt;
+                    B.vu_acc[i] = bits;
+                    B.vu_region[i] = o.region;
+                }
+            }
+        }
+        const uint32_t am = __ballot_sync(0xFFFFFFFFu, adm);
+        const uint32_t gm = __ballot_sync(0xFFFFFFFFu, goal);
+        if ((threadIdx.x & 31) == 0) {
+            B.admit_mask[i >> 5] = am;
+            B.goal_mask[i >> 5] = gm;
+        }
+    }
+    // warp-aggregated then block-aggregated counters
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        n_valid += __shfl_down_sync(0xFFFFFFFFu, n_valid, off);
+        n_adm += __shfl_down_sync(0xFFFFFFFFu, n_adm, off);
+        n_steps += __shfl_down_sync(0xFFFFFFFFu, n_steps, off);
+        n_pts += __shfl_down_sync(0xFFFFFFFFu, n_pts, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_cnt[0], static_cast<unsigned long long>(n_valid));
+        atomicAdd(&s_cnt[1], static_cast<unsigned long long>(n_adm));
+        atomicAdd(&s_cnt[2], static_cast<unsigned long long>(n_steps));
+        atomicAdd(&s_cnt[3], static_cast<unsigned long long>(n_pts));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_cnt[0]) atomicAdd(&ctl->stats.valid, s_cnt[0]);
+        if (s_cnt[1]) atomicAdd(&ctl->stats.admitted, s_cnt[1]);
+        if (s_cnt[2]) atomicAdd(&ctl->stats.rk4_steps, s_cnt[2]);
+        if (s_cnt[3]) atomicAdd(&ctl->stats.points_checked, s_cnt[3]);
+    }
+}
+
+// Block-wide inclusive sum of three counters (blockDim == KP_SELECT_THREADS).
+struct Cnt3 {
+    uint32_t k, v, c;
+};
+
+KP_DEV Cnt3 block_scan3(Cnt3 x, Cnt3* total) {
+    __shared__ uint32_t sw[3][KP_SELECT_THREADS / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Cnt3 inc = x;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, inc.k, off);
+        const uint32_t b = __shfl_up_sync(0xFFFFFFFFu, inc.v, off);
+        const uint32_t c = __shfl_up_sync(0xFFFFFFFFu, inc.c, off);
+        if (lane >= off) { inc.k += a; inc.v += b; inc.c += c; }
+    }
+    if (lane == 31) { sw[0][warp] = inc.k; sw[1][warp] = inc.v; sw[2][warp] = inc.c; }
+    __syncthreads();
+    if (warp == 0) {
+        constexpr int NW = KP_SELECT_THREADS / 32;
+        uint32_t a = lane < NW ? sw[0][lane] : 0, b = lane < NW ? sw[1][lane] : 0, c = lane < NW ? sw[2][lane] : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t a2 = __shfl_up_sync(0xFFFFFFFFu, a, off);
+            const uint32_t b2 = __shfl_up_sync(0xFFFFFFFFu, b, off);
+            const uint32_t c2 = __shfl_up_sync(0xFFFFFFFFu, c, off);
+            if (lane >= off) { a += a2; b += b2; c += c2; }
+        }
+        if (lane < NW) { sw[0][lane] = a; sw[1][lane] = b; sw[2][lane] = c; }
+    }
+    __syncthreads();
+    if (warp > 0) { inc.k += sw[0][warp - 1]; inc.v += sw[1][warp - 1]; inc.c += sw[2][warp - 1]; }
+    total->k = sw[0][KP_SELECT_THREADS / 32 - 1];
+    total->v = sw[1][KP_SELECT_THREADS / 32 - 1];
+    total->c = sw[2][KP_SELECT_THREADS / 32 - 1];
+    __syncthreads();
+    return inc;
+}
+
+// prune_pass rules for one live node (priorities :434-437).
+// Returns the new status; writes status / i_count when they change.
+KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, uint32_t* term, uint32_t* deact,
+                          uint32_t* react) {
+    const uint8_t st = B.status[g];
+    const uint32_t a = B.acc[g];
+    if (a > B.rc[B.region[g]]) {  // (1) dominated -> Terminal (absorbing)
+        B.status[g] = KP_ST_TERMINAL;
+        ++*term;
+        return KP_ST_TERMINAL;
+    }
+    if (st == KP_ST_INACTIVE) {  // (2) inactivity counter, reactivation
+        const uint32_t ic = B.icnt[g] + 1u;
+        if (ic > static_cast<uint32_t>(P.i_max)) {
+            B.icnt[g] = 0;
+            B.status[g] = KP_ST_ACTIVE;
+            ++*react;
+            return KP_ST_ACTIVE;
+        }
+        B.icnt[g] = static_cast<uint16_t>(ic);
+        return KP_ST_INACTIVE;
+    }
+    // (3) Active: some ancestor no longer region-minimal -> Inactive
+    bool dominated = P.deact != 0;
+    int32_t p = B.parent[g];
+    while (!dominated && p >= 0) {
+        if (B.acc[p] > B.rc[B.region[p]]) dominated = true;
+        p = B.parent[p];
+    }
+    if (dominated) {
+        B.status[g] = KP_ST_INACTIVE;
+        B.icnt[g] = 0;
+        ++*deact;
+        return KP_ST_INACTIVE;
+    }
+    return KP_ST_ACTIVE;
+}
+
+__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P, KpBuffers B) {
+    KpCtl* ctl = B.ctl;
+    if (ctl->done) return;
+    __shared__ unsigned int s_last;
+    __shared__ uint32_t s_st[3];
+    const uint32_t it = ctl->iter;
+    const uint32_t n_live = ctl->n_live;
+    const uint32_t live_pad = (n_live + 31u) & ~31u;
+    const uint32_t n_items = ctl->n_items;
+    const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
+    const uint32_t n_tiles = (E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
+    const uint32_t* __restrict__ live = B.live[it & 1];
+    uint32_t term = 0, deact = 0, react = 0;
+    if (threadIdx.x < 3) s_st[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
+        Cnt3 x{0, 0, 0};
+        bool commit = false;
+        if (e < n_live) {
+            const uint8_t st = prune_node(P, B, live[e], &term, &deact, &react);
+            x.k = st != KP_ST_TERMINAL;
+            x.v = st == KP_ST_ACTIVE;
+        } else if (e >= live_pad && e < E) {
+            const uint32_t s = e - live_pad;
+            if (s < n_items && ((B.admit_mask[s >> 5] >> (s & 31)) & 1u)) {
+                commit = B.vu_acc[s] == B.rc[B.vu_region[s]];  // Alg. 4 line 3, bit-exact
+                x.c = commit;
+            }
+        }
+        // slot elements are warp-aligned (live part padded to 32)
+        const uint32_t cm = __ballot_sync(0xFFFFFFFFu, commit);
+        if (e >= live_pad && e < E && (threadIdx.x & 31) == 0) B.commit_mask[(e - live_pad) >> 5] = cm;
+        Cnt3 tot;
+        block_scan3(x, &tot);
+        if (threadIdx.x == 0) {
+            B.tile_sums[tile] = tot.k;
+            B.tile_sums[B.max_tiles + tile] = tot.v;
+            B.tile_sums[2 * B.max_tiles + tile] = tot.c;
+        }
+    }
+    if (term) atomicAdd(&s_st[0], term);
+    if (deact) atomicAdd(&s_st[1], deact);
+    if (react) atomicAdd(&s_st[2], react);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_st[0]) atomicAdd(&ctl->stats.pruned_terminal, static_cast<unsigned long long>(s_st[0]));
+        if (s_st[1]) atomicAdd(&ctl->stats.deactivated, static_cast<unsigned long long>(s_st[1]));
+        if (s_st[2]) atomicAdd(&ctl->stats.reactivated, static_cast<unsigned long long>(s_st[2]));
+        __threadfence();
+        s_last = (atomicAdd(&ctl->ticket_a, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // last block: exclusive scan of the tile counts.  Each thread owns a
+    // contiguous chunk of tiles: sequential sum, one block scan, sequential write.
+    const uint32_t chunk = (n_tiles + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
+    const uint32_t t0 = threadIdx.x * chunk;
+    const uint32_t t1 = min(t0 + chunk, n_tiles);
+    Cnt3 x{0, 0, 0};
+    for (uint32_t t = t0; t < t1; ++t) {
+        x.k += B.tile_sums[t];
+        x.v += B.tile_sums[B.max_tiles + t];
+        x.c += B.tile_sums[2 * B.max_tiles + t];
+    }
+    Cnt3 carry;
+    const Cnt3 inc = block_scan3(x, &carry);
+    Cnt3 run{inc.k - x.k, inc.v - x.v, inc.c - x.c};
+    for (uint32_t t = t0; t < t1; ++t) {
+        const uint32_t a = B.tile_sums[t], b = B.tile_sums[B.max_tiles + t], c = B.tile_sums[2 * B.max_tiles + t];
+        B.tile_prefix[t] = run.k;
+        B.tile_prefix[B.max_tiles + t] = run.v;
+        B.tile_prefix[2 * B.max_tiles + t] = run.c;
+        run.k += a; run.v += b; run.c += c;
+    }
+    if (threadIdx.x == 0) {
+        const uint32_t remaining = P.capacity - ctl->n_nodes;
+        ctl->n_tiles = n_tiles;
+        ctl->tot_keep = carry.k;
+        ctl->tot_va = carry.v;
+        ctl->tot_commit = carry.c;
+        ctl->accepted = carry.c < remaining ? carry.c : remaining;
+        ctl->ticket_a = 0;
+        __threadfence();
+    }
+}
+
+__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem P, KpBuffers B) {
+    KpCtl* ctl = B.ctl;
+    if (ctl->done) return;
+    __shared__ unsigned int s_last;
+    const uint32_t it = ctl->iter;
+    const uint32_t n_live = ctl->n_live;
+    const uint32_t live_pad = (n_live + 31u) & ~31u;
+    const uint32_t n_items = ctl->n_items;
+    const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
+    const uint32_t n_tiles = ctl->n_tiles;
+    const uint32_t tot_keep = ctl->tot_keep, tot_va = ctl->tot_va, accepted = ctl->accepted;
+    const uint32_t n_nodes = ctl->n_nodes;
+    const uint32_t cap = P.capacity, S = P.max_slots;
+    const uint32_t lam = static_cast<uint32_t>(P.lambda);
+    const uint32_t* __restrict__ live = B.live[it & 1];
+    const uint32_t* __restrict__ va = B.va[it & 1];
+    uint32_t* __restrict__ live_n = B.live[(it + 1) & 1];
+    uint32_t* __restrict__ va_n = B.va[(it + 1) & 1];
+    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
+        Cnt3 x{0, 0, 0};
+        uint32_t g = 0, s = 0;
+        bool is_live = false, is_slot = false;
+        if (e < n_live) {
+            is_live = true;
+            g = live[e];
+            const uint8_t st = B.status[g];
+            x.k = st != KP_ST_TERMINAL;
+            x.v = st == KP_ST_ACTIVE;
+        } else if (e >= live_pad && e < E) {
+            s = e - live_pad;
+            if (s < n_items) {
+                is_slot = true;
+                x.c = (B.commit_mask[s >> 5] >> (s & 31)) & 1u;
+            }
+        }
+        Cnt3 tot;
+        const Cnt3 inc = block_scan3(x, &tot);
+        const uint32_t pk = B.tile_prefix[tile] + inc.k - x.k;
+        const uint32_t pv = B.tile_prefix[B.max_tiles + tile] + inc.v - x.v;
+        const uint32_t pc = B.tile_prefix[2 * B.max_tiles + tile] + inc.c - x.c;
+        if (is_live && x.k) {
+            live_n[pk] = g;
+            if (x.v) va_n[pv] = g;
+        }
+        if (is_slot && x.c && pc < accepted) {
+            const uint32_t id = n_nodes + pc;
+#pragma unroll 4
+            for (int d = 0; d < P.n; ++d)
+                B.state[static_cast<size_t>(d) * cap + id] = B.vu_state[static_cast<size_t>(d) * S + s];
+#pragma unroll 4
+            for (int d = 0; d < P.m; ++d)
+                B.ctrl[static_cast<size_t>(d) * cap + id] = B.vu_ctrl[static_cast<size_t>(d) * S + s];
+            const uint32_t abits = B.vu_acc[s];
+            B.dt[id] = B.vu_dt[s];
+            B.acc[id] = abits;
+            B.region[id] = B.vu_region[s];
+            B.parent[id] = static_cast<int32_t>(va[s / lam]);
+            B.status[id] = KP_ST_ACTIVE;
+            B.icnt[id] = 0;
+            live_n[tot_keep + pc] = id;
+            va_n[tot_va + pc] = id;
+            if ((B.goal_mask[s >> 5] >> (s & 31)) & 1u)  // Alg. 4 lines 5-7
+                atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(&ctl->ticket_b, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    // ---- iteration boundary ----
+    const unsigned long long now = globaltimer();
+    const uint32_t it1 = it + 1;
+    ctl->stats.attempted += n_items;
+    ctl->stats.committed += accepted;
+    if (ctl->tot_commit > accepted) {
+        ctl->stats.dropped_capacity += ctl->tot_commit - accepted;
+        ctl->capacity_exhausted = 1;
+    }
+    ctl->n_nodes = n_nodes + accepted;
+    ctl->n_live = tot_keep + accepted;
+    ctl->n_va = tot_va + accepted;
+    const unsigned long long items = static_cast<unsigned long long>(ctl->n_va) * lam;
+    ctl->iter = it1;
+    ctl->t_last_ns = now;
+    const unsigned long long best = ctl->best;
+    const unsigned long long prev = ctl->timeline_len ? ctl->timeline[ctl->timeline_len - 1].best : ~0ull;
+    if (best < prev) {  // strict improvement at this iteration boundary (cost bits are the high word)
+        if (ctl->timeline_len < KP_TIMELINE_CAP) {
+            KpTimeline& t = ctl->timeline[ctl->timeline_len];
+            t.iteration = it1;
+            t.t_ns = now - ctl->t_start_ns;
+            t.best = best;
+            ctl->timeline_len += 1;
+        }
+        if (ctl->first_ns == 0) {
+            ctl->first_ns = now - ctl->t_start_ns;
+            ctl->first_iter = it1;
+        }
+        ctl->best_ns = now - ctl->t_start_ns;
+        ctl->best_iter = it1;
+    }
+    bool done = false;
+    if (items > S) {
+        ctl->error = 8;  // KP_ERR_SLOT_OVERFLOW
+        done = true;
+        ctl->n_items = 0;
+    } else {
+        ctl->n_items = static_cast<uint32_t>(items);
+    }
+    if (ctl->max_iter_abs && it1 >= ctl->max_iter_abs) done = true;
+    if (ctl->deadline_ns && now >= ctl->deadline_ns) done = true;
+    if (ctl->stop_first && best != ~0ull) done = true;
+    if (ctl->n_live == 0) done = true;
+    ctl->ticket_b = 0;
+    if (done) {
+        ctl->done = 1;
+        __threadfence_system();
+        *B.host_done = 1;
+    }
+    __threadfence_system();
+}
+
+// Reset the region table and plant the root (Alg. 1 lines 1-5).
+__global__ void k_reset_table(KpProblem P, KpBuffers B) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_regions; i += gridDim.x * blockDim.x)
+        B.rc[i] = 0x7F800000u;
+}
+
+__global__ void k_reset_root(KpProblem P, KpBuffers B, unsigned long long seed) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    KpCtl* ctl = B.ctl;
+    ctl->seed = seed;
+    float x[KP_MAX_N];
+    for (int d = 0; d < P.n; ++d) {
+        x[d] = P.x_init[d];
+        B.state[static_cast<size_t>(d) * P.capacity] = x[d];
+    }
+    for (int d = 0; d < P.m; ++d) B.ctrl[static_cast<size_t>(d) * P.capacity] = 0.0f;
+    const uint32_t r = region_index<KP_MAX_N>(P, x);
+    B.dt[0] = 0.0f;
+    B.acc[0] = 0u;
+    B.parent[0] = -1;
+    B.region[0] = r;
+    B.status[0] = KP_ST_ACTIVE;
+    B.icnt[0] = 0;
+    B.rc[r] = 0u;  // DECISION: root region seeded with cost 0 (SPEC.md:425 region dominance)
+    B.live[0][0] = 0;
+    B.va[0][0] = 0;
+    ctl->n_live = 1;
+    ctl->n_va = 1;
+    ctl->n_nodes = 1;
+    ctl->n_items = static_cast<uint32_t>(P.lambda);
+    ctl->best = ~0ull;
+}
+
+// Start of a kp_solve call: budget, iteration cap, immediate termination test.
+__global__ void k_start(KpBuffers B, unsigned long long budget_ns, uint32_t max_iters, uint32_t stop_first) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    KpCtl* ctl = B.ctl;
+    const unsigned long long now = globaltimer();
+    if (ctl->iter == 0 && ctl->t_start_ns == 0) ctl->t_start_ns = now;
+    ctl->deadline_ns = budget_ns ? now + budget_ns : 0ull;
+    ctl->max_iter_abs = max_iters ? ctl->iter + max_iters : 0u;
+    ctl->stop_first = stop_first;
+    ctl->ticket_a = 0;
+    ctl->ticket_b = 0;
+    bool done = ctl->error != 0 || ctl->n_live == 0 || (stop_first && ctl->best != ~0ull);
+    ctl->done = done ? 1u : 0u;
+    __threadfence_system();
+    *B.host_done = done ? 1u : 0u;
+    __threadfence_system();
+}
+
+// Explicit-input propagate items (kp_debug_propagate).
+template <int MODEL>
+__global__ void k_debug_propagate(KpProblem P, KpBuffers B, uint32_t n, const float* ps, const float* pacc,
+                                  const uint32_t* ids, const uint32_t* brs, uint32_t it, uint8_t* valid,
+                                  float* xs, float* us, float* dts, float* accs, uint32_t* regs, uint32_t* steps,
+                                  uint8_t* goals) {
+    constexpr int N = Model<MODEL>::N;
+    constexpr int M = Model<MODEL>::M;
+    extern __shared__ float smem[];
+    stage_obstacles(P, B, smem, smem + 6 * P.n_box);
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float x[N], u[M], dt;
+    for (int d = 0; d < N; ++d) x[d] = ps[static_cast<size_t>(i) * N + d];
+    ItemOut o;
+    const int rc = propagate_item<MODEL>(P, smem, smem + 6 * P.n_box, x, pacc[i], B.ctl->seed, it, ids[i], brs[i], u, dt, o);
+    valid[i] = rc == 0 ? 1 : (rc == 1 ? 0 : 2);
+    for (int d = 0; d < N; ++d) xs[static_cast<size_t>(i) * N + d] = rc == 0 ? x[d] : 0.0f;
+    for (int d = 0; d < M; ++d) us[static_cast<size_t>(i) * M + d] = u[d];
+    dts[i] = dt;
+    accs[i] = rc == 0 ? o.acc : 0.0f;
+    regs[i] = rc == 0 ? o.region : 0u;
+    steps[i] = o.steps;
+    goals[i] = rc == 0 ? o.goal : 0;
+}
+
+// extract_trajectory, step 1: root->leaf chain on the device.
+__global__ void k_chain(KpBuffers B, int32_t leaf, int32_t* chain, uint32_t cap, uint32_t* len) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint32_t n = 0;
+    for (int32_t p = leaf; p >= 0; p = B.parent[p]) ++n;
+    *len = n;
+    uint32_t k = n;
+    for (int32_t p = leaf; p >= 0; p = B.parent[p]) {
+        --k;
+        if (k < cap) chain[k] = p;
+    }
+}
+
+// Step 1b: gather the chain's node records into compact row-major buffers.
+__global__ void k_gather_chain(KpProblem P, KpBuffers B, const int32_t* chain, uint32_t len, float* st, float* ct,
+                               float* dts, float* accs) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= len) return;
+    const uint32_t g = static_cast<uint32_t>(chain[j]);
+    for (int d = 0; d < P.n; ++d) st[static_cast<size_t>(j) * P.n + d] = B.state[static_cast<size_t>(d) * P.capacity + g];
+    for (int d = 0; d < P.m; ++d) ct[static_cast<size_t>(j) * P.m + d] = B.ctrl[static_cast<size_t>(d) * P.capacity + g];
+    dts[j] = B.dt[g];
+    accs[j] = __uint_as_float(B.acc[g]);
+}
+
+// Step 2: re-integrate segment j (chain[j] -> chain[j+1]) with the exact
+// propagate arithmetic; samples 1..S of each segment at out[off[j] ..].
+template <int MODEL>
+__global__ void k_reintegrate(KpProblem P, KpBuffers B, const int32_t* chain, uint32_t n_seg, const uint32_t* off,
+                              float* out, float* seg_cost) {
+    constexpr int N = Model<MODEL>::N;
+    constexpr int M = Model<MODEL>::M;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_seg) return;
+    const uint32_t a = static_cast<uint32_t>(chain[j]), b = static_cast<uint32_t>(chain[j + 1]);
+    float x[N], u[M];
+    for (int d = 0; d < N; ++d) x[d] = B.state[static_cast<size_t>(d) * P.capacity + a];
+    for (int d = 0; d < M; ++d) u[d] = B.ctrl[static_cast<size_t>(d) * P.capacity + b];
+    const float dt = B.dt[b];
+    const float q = dt / P.h;
+    int S = static_cast<int>(ceilf(q));
+    if (S < 1) S = 1;
+    float total = 0.0f;
+    float px = x[0], py = x[1], pz = N >= 3 && MODEL != 0 ? x[2] : 0.0f;
+    uint32_t w = off[j];
+    for (int s = 0; s < S; ++s) {
+        const float hk = (s + 1 < S) ? P.h : dt - static_cast<float>(S - 1) * P.h;
+        if (!(hk > 0.0f)) break;
+        rk4_step<MODEL>(P, x, u, hk);
+        for (int d = 0; d < N; ++d) out[static_cast<size_t>(w) * N + d] = x[d];
+        ++w;
+        const float nx = x[0], ny = x[1], nz = MODEL != 0 ? x[2] : 0.0f;
+        const float dx = nx - px, dy = ny - py, dz = nz - pz;
+        float d2 = dx * dx;
+        d2 = fmaf(dy, dy, d2);
+        if (MODEL != 0) d2 = fmaf(dz, dz, d2);
+        total += sqrtf(d2);
+        px = nx; py = ny; pz = nz;
+    }
+    seg_cost[j] = P.cost_kind == 1 ? dt : (total == 0.0f ? P.zero_rate * dt : total);
+}
+
+}  // namespace kp
+
+// ------------------------------------------------------------------------
+// Launch wrappers (C++ linkage, used by kp_capi.cpp).
+// ------------------------------------------------------------------------
+namespace kp {
+
+size_t propagate_smem(const KpProblem& P) { return sizeof(float) * (6 * P.n_box + 4 * P.n_sph); }
+
+cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_prop, int grid_sel, cudaStream_t st,
+                             int which) {
+    const size_t smem = propagate_smem(P);
+    if (which & 1) {
+        switch (P.model) {
+            case 0: k_propagate<0><<<grid_prop, 256, smem, st>>>(P, B); break;
+            case 1: k_propagate<1><<<grid_prop, 256, smem, st>>>(P, B); break;
+            case 2: k_propagate<2><<<grid_prop, 256, smem, st>>>(P, B); break;
+            default: k_propagate<3><<<grid_prop, 256, smem, st>>>(P, B); break;
+        }
+    }
+    if (which & 2) k_select_reduce<<<grid_sel, KP_SELECT_THREADS, 0, st>>>(P, B);
+    if (which & 4) k_select_scatter<<<grid_sel, KP_SELECT_THREADS, 0, st>>>(P, B);
+    return cudaGetLastError();
+}
+
+cudaError_t set_propagate_smem(const KpProblem& P) {
+    const int smem = static_cast<int>(propagate_smem(P));
+    if (smem <= 48 * 1024) return cudaSuccess;
+    cudaError_t e = cudaSuccess;
+    switch (P.model) {
+        case 0: e = cudaFuncSetAttribute(k_propagate<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 1: e = cudaFuncSetAttribute(k_propagate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 2: e = cudaFuncSetAttribute(k_propagate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        default: e = cudaFuncSetAttribute(k_propagate<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+    }
+    return e;
+}
+
+int propagate_occupancy(const KpProblem& P) {
+    int nb = 0;
+    const size_t smem = propagate_smem(P);
+    switch (P.model) {
+        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<0>, 256, smem); break;
+        case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<1>, 256, smem); break;
+        case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<2>, 256, smem); break;
+        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<3>, 256, smem); break;
+    }
+    return nb;
+}
+
+cudaError_t launch_reset(const KpProblem& P, const KpBuffers& B, unsigned long long seed, cudaStream_t st) {
+    cudaMemsetAsync(B.ctl, 0, sizeof(KpCtl), st);
+    k_reset_table<<<148 * 4, 256, 0, st>>>(P, B);
+    k_reset_root<<<1, 32, 0, st>>>(P, B, seed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_start(const KpBuffers& B, unsigned long long budget_ns, uint32_t max_iters, uint32_t stop_first,
+                         cudaStream_t st) {
+    k_start<<<1, 32, 0, st>>>(B, budget_ns, max_iters, stop_first);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_propagate(const KpProblem& P, const KpBuffers& B, uint32_t n, const float* ps,
+                                   const float* pacc, const uint32_t* ids, const uint32_t* brs, uint32_t it,
+                                   uint8_t* valid, float* xs, float* us, float* dts, float* accs, uint32_t* regs,
+                                   uint32_t* steps, uint8_t* goals, cudaStream_t st) {
+    const size_t smem = propagate_smem(P);
+    const int grid = static_cast<int>((n + 127) / 128);
+    if (n == 0) return cudaSuccess;
+    switch (P.model) {
+        case 0: k_debug_propagate<0><<<grid, 128, smem, st>>>(P, B, n, ps, pacc, ids, brs, it, valid, xs, us, dts, accs, regs, steps, goals); break;
+        case 1: k_debug_propagate<1><<<grid, 128, smem, st>>>(P, B, n, ps, pacc, ids, brs, it, valid, xs, us, dts, accs, regs, steps, goals); break;
+        case 2: k_debug_propagate<2><<<grid, 128, smem, st>>>(P, B, n, ps, pacc, ids, brs, it, valid, xs, us, dts, accs, regs, steps, goals); break;
+        default: k_debug_propagate<3><<<grid, 128, smem, st>>>(P, B, n, ps, pacc, ids, brs, it, valid, xs, us, dts, accs, regs, steps, goals); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chain(const KpBuffers& B, int32_t leaf, int32_t* chain, uint32_t cap, uint32_t* len,
+                         cudaStream_t st) {
+    k_chain<<<1, 32, 0, st>>>(B, leaf, chain, cap, len);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_chain(const KpProblem& P, const KpBuffers& B, const int32_t* chain, uint32_t len,
+                                float* st, float* ct, float* dts, float* accs, cudaStream_t s) {
+    if (len == 0) return cudaSuccess;
+    k_gather_chain<<<(len + 127) / 128, 128, 0, s>>>(P, B, chain, len, st, ct, dts, accs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reintegrate(const KpProblem& P, const KpBuffers& B, const int32_t* chain, uint32_t n_seg,
+                               const uint32_t* off, float* out, float* seg_cost, cudaStream_t st) {
+    if (n_seg == 0) return cudaSuccess;
+    const int grid = static_cast<int>((n_seg + 127) / 128);
+    switch (P.model) {
+        case 0: k_reintegrate<0><<<grid, 128, 0, st>>>(P, B, chain, n_seg, off, out, seg_cost); break;
+        case 1: k_reintegrate<1><<<grid, 128, 0, st>>>(P, B, chain, n_seg, off, out, seg_cost); break;
+        case 2: k_reintegrate<2><<<grid, 128, 0, st>>>(P, B, chain, n_seg, off, out, seg_cost); break;
+        default: k_reintegrate<3><<<grid, 128, 0, st>>>(P, B, chain, n_seg, off, out, seg_cost); break;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace kp

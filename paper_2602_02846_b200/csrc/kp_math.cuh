@@ -1,0 +1,350 @@
+// kp_math.cuh — per-work-item device arithmetic of the Kino-PAX+ iteration.
+//
+// This is the pinned fp32 operation recipe of DESIGN.md §4.  The whole
+// library is compiled with --fmad=false, so `a * b + c` is two roundings and
+// only the explicit fmaf() calls below fuse; division and sqrt are IEEE
+// (-prec-div/-prec-sqrt defaults, no fast-math, no FTZ).  Under that recipe a
+// work item's verdict, region, cost bits and final state are bit-identical to
+// the reference restatement run in fp32 (oracle Mirror32 policy).
+//
+// Reference behaviour followed (file:line):
+//   sampling      rng.hpp:12-57
+//   dynamics      model.hpp:42 (derivative)
+//   integrator    SPEC.md:132-140, :163-171; wrap_angle types.hpp:49-58
+//   validity      SPEC.md:200-218, :236-237; contains types.hpp:22-39
+//   cost          cost.hpp:44-67 (segment_cost), :77-84 (in_goal)
+//   region
+#pragma once
+#include <stdint.h>
+
+#include "kp_types.h"
+
+#define KP_DEV __device__ __forceinline__
+
+namespace kp {
+
+// ------------------------------------------------------------------- RNG ---
+KP_DEV uint64_t mix64(uint64_t z) {  // rng.hpp:34-39
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+KP_DEV uint64_t derive_stream(uint64_t seed, uint64_t it, uint64_t node, uint64_t br) {  // rng.hpp:44-52
+    uint64_t s = mix64(seed);
+    s = mix64(s ^ it);
+    s = mix64(s ^ node);
+    s = mix64(s ^ br);
+    return s;
+}
+
+struct SplitMix64 {  // rng.hpp:12-31
+    uint64_t state;
+    KP_DEV uint64_t next() {
+        state += 0x9E3779B97F4A7C15ULL;
+        uint64_t z = state;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+    KP_DEV double unit() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }  // rng.hpp:55-57
+};
+
+// Philox4x32-10, counter (c0..c3), key (k0, k1).
+KP_DEV uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// sample_control + sample_duration for one work item (controls in axis
+// order, then dt = t_prop * (1 - U) in (0, t_prop]).
+template <int M>
+KP_DEV void sample_item(const KpProblem& P, uint64_t seed, uint32_t it, uint32_t node, uint32_t br, float* u,
+                        float& dt) {
+    if (P.rng_kind == 1) {
+        SplitMix64 r{derive_stream(seed, it, node, br)};
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const double U = r.unit();
+            u[i] = static_cast<float>(P.clo_d[i] + (P.chi_d[i] - P.clo_d[i]) * U);
+        }
+        const double U = r.unit();
+        dt = static_cast<float>(P.t_prop_d * (1.0 - U));
+    } else {
+        const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+        const uint4 a = philox(it, node, br, 0u, k0, k1);
+        uint32_t r[8] = {a.x, a.y, a.z, a.w, 0u, 0u, 0u, 0u};
+        if (M + 1 > 4) {
+            const uint4 b = philox(it, node, br, 1u, k0, k1);
+            r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float U = static_cast<float>(r[i] >> 8) * 0x1.0p-24f;
+            u[i] = fmaf(P.cw[i], U, P.clo[i]);
+        }
+        const float U = static_cast<float>(r[M] >> 8) * 0x1.0p-24f;
+        dt = P.t_prop * (1.0f - U);
+    }
+}
+
+// ----------------------------------------------------------------- math ---
+// Pinned sincos recipe, identical to the oracle's.
+KP_DEV void sincos_recipe(float x, float& s_out, float& c_out) {
+    const float j = rintf(x * 0x1.45f306p-1f);
+    const int q = static_cast<int>(j);
+    float r = fmaf(-j, 0x1.921fb4p+0f, x);
+    r = fmaf(-j, 0x1.4442d2p-24f, r);
+    const float r2 = r * r;
+    float ps = fmaf(r2, 0x1.71de3ap-19f, -0x1.a01a02p-13f);
+    ps = fmaf(r2, ps, 0x1.111112p-7f);
+    ps = fmaf(r2, ps, -0x1.555556p-3f);
+    const float s = fmaf(r * r2, ps, r);
+    float pc = fmaf(r2, -0x1.27e4fcp-22f, 0x1.a01a02p-16f);
+    pc = fmaf(r2, pc, -0x1.6c16c2p-10f);
+    pc = fmaf(r2, pc, 0x1.555556p-5f);
+    pc = fmaf(r2, pc, -0.5f);
+    const float c = fmaf(r2, pc, 1.0f);
+    switch (q & 3) {
+        case 0: s_out = s; c_out = c; break;
+        case 1: s_out = c; c_out = -s; break;
+        case 2: s_out = -s; c_out = -c; break;
+        default: s_out = -c; c_out = s; break;
+    }
+}
+
+// wrap_angle (types.hpp:49-58) in fp32; only called outside (-pi, pi], where
+// fmodf is exact, so the result equals calling it unconditionally.
+KP_DEV float wrap_angle(float a) {
+    const float pi = 3.14159265358979323846f;
+    if (a > pi || a <= -pi) {
+        a = fmodf(a, 2.0f * pi);
+        if (a <= -pi) a += 2.0f * pi;
+        else if (a > pi) a -= 2.0f * pi;
+    }
+    return a;
+}
+
+// ------------------------------------------------------------ dynamics ----
+template <int MODEL> struct Model;
+template <> struct Model<0> { static constexpr int N = 4, M = 2, NA = 0, A0 = 0; };   // double_integrator_4d
+template <> struct Model<1> { static constexpr int N = 6, M = 3, NA = 0, A0 = 0; };   // double_integrator_6d
+template <> struct Model<2> { static constexpr int N = 6, M = 3, NA = 1, A0 = 3; };   // dubins_airplane_6d (psi)
+template <> struct Model<3> { static constexpr int N = 12, M = 4, NA = 3, A0 = 6; };  // quadcopter_12d (phi,theta,psi)
+
+// DynamicsModel::derivative (model.hpp:42).
+template <int MODEL>
+KP_DEV void derivative(const KpProblem& P, const float* x, const float* u, float* f) {
+    if constexpr (MODEL == 0) {
+        f[0] = x[2]; f[1] = x[3]; f[2] = u[0]; f[3] = u[1];
+    } else if constexpr (MODEL == 1) {
+        f[0] = x[3]; f[1] = x[4]; f[2] = x[5]; f[3] = u[0]; f[4] = u[1]; f[5] = u[2];
+    } else if constexpr (MODEL == 2) {
+        float sp, cp, sg, cg;
+        sincos_recipe(x[3], sp, cp);
+        sincos_recipe(x[4], sg, cg);
+        const float vc = x[5] * cg;
+        f[0] = vc * cp; f[1] = vc * sp; f[2] = x[5] * sg;
+        f[3] = u[0]; f[4] = u[1]; f[5] = u[2];
+    } else {
+        float sph, cph, sth, cth, sps, cps;
+        sincos_recipe(x[6], sph, cph);
+        sincos_recipe(x[7], sth, cth);
+        sincos_recipe(x[8], sps, cps);
+        const float a = u[0] * P.inv_m;
+        const float t1 = cph * sth;
+        f[0] = x[3]; f[1] = x[4]; f[2] = x[5];
+        f[3] = a * fmaf(t1, cps, sph * sps);
+        f[4] = a * fmaf(t1, sps, -(sph * cps));
+        f[5] = fmaf(a, cph * cth, -P.grav);
+        const float w = fmaf(x[10], sph, x[11] * cph);
+        f[6] = fmaf(w, sth / cth, x[9]);
+        f[7] = fmaf(x[10], cph, -(x[11] * sph));
+        f[8] = w / cth;
+        f[9] = fmaf(P.cx, x[10] * x[11], u[1] * P.inv_ix);
+        f[10] = fmaf(P.cy, x[9] * x[11], u[2] * P.inv_iy);
+        f[11] = fmaf(P.cz, x[9] * x[10], u[3] * P.inv_iz);
+    }
+}
+
+// One classical RK4 step with constant control, then angle wrap.
+// Returns false when a coordinate is non-finite (propagation diverged).
+template <int MODEL>
+KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk) {
+    constexpr int N = Model<MODEL>::N;
+    float k1[N], k2[N], k3[N], k4[N], t[N];
+    const float half = 0.5f * hk;
+    derivative<MODEL>(P, x, u, k1);
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] = fmaf(half, k1[i], x[i]);
+    derivative<MODEL>(P, t, u, k2);
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] = fmaf(half, k2[i], x[i]);
+    derivative<MODEL>(P, t, u, k3);
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] = fmaf(hk, k3[i], x[i]);
+    derivative<MODEL>(P, t, u, k4);
+    const float sixth = hk / 6.0f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const float a = k1[i] + k4[i];
+        const float b = k2[i] + k3[i];
+        x[i] = fmaf(sixth, fmaf(2.0f, b, a), x[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < Model<MODEL>::NA; ++i) x[Model<MODEL>::A0 + i] = wrap_angle(x[Model<MODEL>::A0 + i]);
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) ok = ok && isfinite(x[i]);
+    return ok;
+}
+
+// --------------------------------------------------------- environment ----
+// Position outside every closed obstacle?  Obstacles staged in shared memory;
+// every lane reads the same primitive at the same time (broadcast).
+KP_DEV bool in_obstacle(const float* __restrict__ sbox, int n_box, const float* __restrict__ ssph, int n_sph,
+                        float px, float py, float pz) {
+    for (int b = 0; b < n_box; ++b) {
+        const float* o = sbox + 6 * b;
+        if (px >= o[0] && px <= o[3] && py >= o[1] && py <= o[4] && pz >= o[2] && pz <= o[5]) return true;
+    }
+    for (int s = 0; s < n_sph; ++s) {
+        const float* o = ssph + 4 * s;
+        const float dx = px - o[0], dy = py - o[1], dz = pz - o[2];
+        float d2 = dx * dx;
+        d2 = fmaf(dy, dy, d2);
+        d2 = fmaf(dz, dz, d2);
+        if (d2 <= o[3]) return true;
+    }
+    return false;
+}
+
+// is_state_valid minus the obstacle part, which the caller
+// does on the (px, py, pz) projection.
+template <int MODEL>
+KP_DEV bool within_bounds(const KpProblem& P, const float* x) {
+    constexpr int N = Model<MODEL>::N;
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) ok = ok && (x[i] >= P.slo[i]) && (x[i] <= P.shi[i]);
+    constexpr int W = (MODEL == 0) ? 2 : 3;
+#pragma unroll
+    for (int i = 0; i < W; ++i) ok = ok && (x[i] >= P.wlo[i]) && (x[i] <= P.whi[i]);
+    return ok;
+}
+
+// x[d] for a runtime d without spilling x to local memory (fully unrolled select).
+template <int N>
+KP_DEV float pick(const float* x, int d) {
+    float v = x[0];
+#pragma unroll
+    for (int k = 1; k < N; ++k) v = (d == k) ? x[k] : v;
+    return v;
+}
+
+// region_index.
+template <int N>
+KP_DEV uint32_t region_index(const KpProblem& P, const float* x) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < KP_MAX_GRID; ++j) {
+        if (j >= P.grid_n) break;
+        const float v = (pick<N>(x, P.grid_dims[j]) - P.g_lo[j]) / P.g_side[j];
+        const float fv = floorf(v);
+        uint32_t i;
+        if (fv < 0.0f) i = 0;
+        else if (fv > static_cast<float>(P.g_cells[j] - 1)) i = static_cast<uint32_t>(P.g_cells[j] - 1);
+        else i = static_cast<uint32_t>(fv);
+        r += i * P.g_stride[j];
+    }
+    return r;
+}
+
+// in_goal (cost.hpp:77-84), boundary inclusive.
+template <int N>
+KP_DEV bool in_goal(const KpProblem& P, const float* x) {
+    float d = pick<N>(x, P.goal_dims[0]) - P.goal_c[0];
+    float d2 = d * d;
+#pragma unroll
+    for (int i = 1; i < N; ++i) {
+        if (i >= P.goal_n) break;
+        d = pick<N>(x, P.goal_dims[i]) - P.goal_c[i];
+        d2 = fmaf(d, d, d2);
+    }
+    return d2 <= P.goal_r2;
+}
+
+// --------------------------------------------------------- work item ------
+struct ItemOut {
+    float acc;
+    uint32_t region;
+    uint32_t steps;
+    uint32_t points;
+    bool goal;
+};
+
+// One work item of Alg. 2 lines 3-7: sample (u, dt), RK4
+// rollout streamed in registers, every sample validated and every
+// interpolated point (spacing <= collision_step) obstacle-checked, path length
+// accumulated, region of the end state.  x holds the parent state on entry and
+// the candidate state on a valid exit.  Returns 0 valid, 1 invalid, 2 diverged.
+// The parent (samples[0]) is not re-checked: it is a stored valid node.
+template <int MODEL>
+KP_DEV int propagate_item(const KpProblem& P, const float* __restrict__ sbox, const float* __restrict__ ssph,
+                          float* x, float acc_parent, uint64_t seed, uint32_t it, uint32_t node, uint32_t br,
+                          float* u, float& dt, ItemOut& o) {
+    constexpr int M = Model<MODEL>::M;
+    constexpr bool TWO_D = (MODEL == 0);
+    sample_item<M>(P, seed, it, node, br, u, dt);
+    const float q = dt / P.h;
+    int S = static_cast<int>(ceilf(q));
+    if (S < 1) S = 1;
+    float px = x[0], py = x[1], pz = TWO_D ? 0.0f : x[2];
+    float total = 0.0f;
+    o.steps = 0;
+    o.points = 0;
+    for (int s = 0; s < S; ++s) {
+        const float hk = (s + 1 < S) ? P.h : dt - static_cast<float>(S - 1) * P.h;
+        if (!(hk > 0.0f)) break;
+        if (!rk4_step<MODEL>(P, x, u, hk)) return 2;
+        o.steps += 1;
+        const float nx = x[0], ny = x[1], nz = TWO_D ? 0.0f : x[2];
+        o.points += 1;
+        if (!within_bounds<MODEL>(P, x)) return 1;
+        if (in_obstacle(sbox, P.n_box, ssph, P.n_sph, nx, ny, nz)) return 1;
+        const float dx = nx - px, dy = ny - py, dz = nz - pz;
+        float d2 = dx * dx;
+        d2 = fmaf(dy, dy, d2);
+        if (!TWO_D) d2 = fmaf(dz, dz, d2);
+        const float d = sqrtf(d2);
+        if (d > P.coll) {
+            const int k = static_cast<int>(ceilf(d / P.coll));
+            for (int j = 1; j < k; ++j) {
+                const float t = static_cast<float>(j) / static_cast<float>(k);
+                o.points += 1;
+                if (in_obstacle(sbox, P.n_box, ssph, P.n_sph, fmaf(t, dx, px), fmaf(t, dy, py),
+                                TWO_D ? 0.0f : fmaf(t, dz, pz)))
+                    return 1;
+            }
+        }
+        total += d;  // cost.hpp:59-61 (position head == workspace dims for every built-in model)
+        px = nx; py = ny; pz = nz;
+    }
+    float seg;
+    if (P.cost_kind == 1) seg = dt;                        // control_duration
+    else seg = (total == 0.0f) ? P.zero_rate * dt : total;  // cost.hpp:62
+    o.acc = acc_parent + seg;
+    o.region = region_index<Model<MODEL>::N>(P, x);
+    o.goal = in_goal<Model<MODEL>::N>(P, x);
+    return 0;
+}
+
+}  // namespace kp

@@ -1,0 +1,127 @@
+// kp_types.h — host/device layout of one B200 planner instance.
+//
+// Everything the kernels read lives in two places:
+//   KpProblem  — immutable problem/config constants, pre-rounded to fp32 on the
+//                host once (the same fp32 constants the Mirror32 recipe uses);
+//                passed to every kernel by value (kernel parameter space).
+//   KpCtl      — the mutable control block in device memory: list sizes,
+//                iteration counter, best solution, stats, timeline, done flag.
+// Node store, region table, V_U slots and the frontier/live lists are separate
+// SoA buffers (KpBuffers) so every per-node field is a coalesced stream.
+#pragma once
+#include <stdint.h>
+
+#define KP_MAX_N 12
+#define KP_MAX_M 4
+#define KP_MAX_GRID 6
+#define KP_TIMELINE_CAP 4096
+#define KP_SELECT_THREADS 256
+#define KP_SELECT_ITEMS 4
+#define KP_SELECT_TILE (KP_SELECT_THREADS * KP_SELECT_ITEMS)
+#define KP_SMEM_OBSTACLES 2048
+
+enum KpStatus : uint8_t { KP_ST_ACTIVE = 0, KP_ST_INACTIVE = 1, KP_ST_TERMINAL = 2 };
+
+struct KpProblem {
+    int32_t model;           // kp_model_id
+    int32_t n, m;            // state / control dims
+    int32_t ws_dim;          // 2 or 3 (device always tests 3-D; 2-D scenes pad z)
+    int32_t n_box, n_sph;
+    int32_t n_angle;
+    int32_t angle_dims[3];
+    int32_t goal_n;
+    int32_t goal_dims[KP_MAX_N];
+    float goal_c[KP_MAX_N];
+    float goal_r2;
+    int32_t cost_kind;       // 0 path length, 1 control duration
+    int32_t cost_pos_dims;
+    float slo[KP_MAX_N], shi[KP_MAX_N];
+    float clo[KP_MAX_M], cw[KP_MAX_M];
+    double clo_d[KP_MAX_M], chi_d[KP_MAX_M];
+    float wlo[3], whi[3];
+    int32_t grid_n;
+    int32_t grid_dims[KP_MAX_GRID];
+    float g_lo[KP_MAX_GRID], g_side[KP_MAX_GRID];
+    int32_t g_cells[KP_MAX_GRID];
+    uint32_t g_stride[KP_MAX_GRID];
+    uint32_t n_regions;
+    float t_prop, h, coll, zero_rate;
+    double t_prop_d;
+    float inv_m, grav, cx, cy, cz, inv_ix, inv_iy, inv_iz;
+    int32_t lambda, i_max, rng_kind, deact;
+    uint32_t capacity;       // t_e
+    uint32_t max_slots;      // V_U slot buffer (multiple of 32)
+    float x_init[KP_MAX_N];
+};
+
+struct KpStats {
+    unsigned long long attempted, valid, admitted, committed;
+    unsigned long long pruned_terminal, deactivated, reactivated, dropped_capacity;
+    unsigned long long rk4_steps, points_checked;  // roofline accounting (valid + invalid items)
+};
+
+struct KpTimeline {
+    unsigned long long iteration;
+    unsigned long long t_ns;
+    unsigned long long best;  // (cost bits << 32) | leaf
+};
+
+struct KpCtl {
+    // current iteration's lists (parity = iter & 1)
+    uint32_t iter;            // iterations completed since reset
+    uint32_t done;            // 1 = stop (budget / iterations / first solution / no live nodes)
+    uint32_t error;           // nonzero = device error (slot overflow)
+    uint32_t n_live, n_va, n_nodes, n_items;
+    uint32_t capacity_exhausted;
+    // produced by select_reduce for select_scatter
+    uint32_t n_tiles;
+    uint32_t tot_keep, tot_va, tot_commit, accepted;
+    uint32_t ticket_a, ticket_b;
+    // run bookkeeping
+    uint32_t max_iter_abs;    // stop when iter >= this (0 = unlimited)
+    uint32_t stop_first;
+    uint32_t timeline_len;
+    uint32_t first_iter, best_iter;
+    unsigned long long seed;  // run seed (kept here so captured graphs survive kp_reset)
+    unsigned long long best;  // (cost bits << 32) | leaf ; init ~0
+    unsigned long long t_start_ns, deadline_ns, t_last_ns;
+    unsigned long long first_ns, best_ns;
+    KpStats stats;
+    KpTimeline timeline[KP_TIMELINE_CAP];
+};
+
+// Device buffer set of one planner.
+struct KpBuffers {
+    // node store, SoA [dim][capacity]
+    float* state;
+    float* ctrl;
+    float* dt;
+    uint32_t* acc;       // fp32 cost bits
+    int32_t* parent;
+    uint32_t* region;
+    uint8_t* status;
+    uint16_t* icnt;
+    // region table [n_regions], encoded fp32 bits (+inf = 0x7F800000)
+    uint32_t* rc;
+    // lists, double-buffered [2][capacity]
+    uint32_t* live[2];
+    uint32_t* va[2];
+    // V_U slots, SoA [dim][max_slots]
+    float* vu_state;
+    float* vu_ctrl;
+    float* vu_dt;
+    uint32_t* vu_acc;
+    uint32_t* vu_region;
+    uint32_t* admit_mask;   // [max_slots/32]
+    uint32_t* goal_mask;    // [max_slots/32]
+    uint32_t* commit_mask;  // [max_slots/32]
+    // select scratch
+    uint32_t* tile_sums;    // [3][max_tiles]
+    uint32_t* tile_prefix;  // [3][max_tiles]
+    uint32_t max_tiles;
+    // obstacles: boxes [n_box][6] (lo xyz, hi xyz), spheres [n_sph][4] (c xyz, r^2)
+    const float* boxes;
+    const float* spheres;
+    KpCtl* ctl;
+    volatile uint32_t* host_done;  // mapped pinned word (device writes 1 at termination)
+};

@@ -1,0 +1,138 @@
+"""GPU vs oracle parity through the C-ABI.
+
+Bar (BASELINE.json north_star): validity verdicts, region indices, control /
+duration draws, accumulated-cost bits and final states are bit-exact against
+the fp32 restatement (oracle Mirror32) on identical inputs; whole planner runs
+are bit-identical to the restatement's workers=1 serial run (node store,
+region table, best solution, timeline, stats except the race-dependent
+`propagations_admitted`).  Against the fp64 reference-faithful planner the
+propagated states agree within 1e-5 relative (fp32 tolerance, north_star).
+"""
+import numpy as np
+import pytest
+
+import kpo
+from paper_2602_02846_b200 import Planner, scenarios
+
+pytestmark = pytest.mark.gpu
+
+SCENES = ["forest_di6", "narrow_dubins6", "building_quad12", "zigzag2d", "free2d"]
+
+
+def _random_parents(s, k, rng):
+    """Valid-ish parent states sampled inside the state bounds."""
+    lo = np.array([b[0] for b in s["problem"]["state_bounds"]], float)
+    hi = np.array([b[1] for b in s["problem"]["state_bounds"]], float)
+    x = lo + (hi - lo) * rng.random((k, len(lo)))
+    x[0] = s["problem"]["x_init"]
+    return x.astype(np.float32)
+
+
+@pytest.mark.parametrize("scene", SCENES)
+@pytest.mark.parametrize("rng_kind", ["philox", "splitmix"])
+def test_work_item_parity_bit_exact(scene, rng_kind):
+    s = scenarios.load(scene, rng=rng_kind, max_slots=1 << 16, capacity=1 << 14)
+    rng = np.random.default_rng(7)
+    k = 4096
+    ps = _random_parents(s, k, rng)
+    pacc = (rng.random(k) * 10).astype(np.float32)
+    ids = rng.integers(0, 1 << 20, k).astype(np.uint32)
+    brs = rng.integers(0, 32, k).astype(np.uint32)
+    with Planner(s, seed=1234) as g:
+        d = g.debug_propagate(ps, pacc, ids, brs, iteration=3)
+    o = kpo.Oracle(s, kpo.MIRROR32, seed=1234).propagate_items(ps.astype(np.float64), pacc.astype(np.float64),
+                                                                 ids, brs, 3)
+    np.testing.assert_array_equal(d["control"].astype(np.float64), o["control"])
+    np.testing.assert_array_equal(d["dt"].astype(np.float64), o["dt"])
+    gv, ov = d["valid"] == 1, o["valid"] == 1
+    np.testing.assert_array_equal(gv, ov)
+    assert gv.sum() > 0
+    np.testing.assert_array_equal(d["region"][gv], o["region"][ov])
+    np.testing.assert_array_equal(d["acc"][gv].astype(np.float64), o["acc"][ov])
+    np.testing.assert_array_equal(d["state"][gv].astype(np.float64), o["state"][ov])
+    np.testing.assert_array_equal(d["goal"][gv], o["goal"][ov])
+    np.testing.assert_array_equal(d["steps"][gv], o["steps"][ov])
+
+
+@pytest.mark.parametrize("scene", ["forest_di6", "narrow_dubins6", "building_quad12"])
+def test_work_item_states_within_1e5_of_fp64(scene):
+    """fp32 device vs the fp64 reference-faithful restatement on identical
+    (u, dt): final states within 1e-5 relative (north_star tolerance)."""
+    s = scenarios.load(scene, rng="splitmix", max_slots=1 << 16, capacity=1 << 14)
+    rng = np.random.default_rng(11)
+    k = 2048
+    ps = _random_parents(s, k, rng)
+    pacc = np.zeros(k, np.float32)
+    ids = rng.integers(0, 1 << 20, k).astype(np.uint32)
+    brs = rng.integers(0, 32, k).astype(np.uint32)
+    with Planner(s, seed=99) as g:
+        d = g.debug_propagate(ps, pacc, ids, brs, iteration=0)
+    o = kpo.Oracle(s, kpo.FAITHFUL64, seed=99)
+    h = float(s["planner"]["ode_step"])
+    worst = 0.0
+    checked = 0
+    for i in range(0, k, 7):
+        if d["valid"][i] != 1:
+            continue
+        ref = o.propagate_ode(ps[i].astype(np.float64), d["control"][i].astype(np.float64),
+                              float(d["dt"][i]), h)[-1]
+        got = d["state"][i].astype(np.float64)
+        scale = np.maximum(np.abs(ref), 1.0)
+        worst = max(worst, float(np.max(np.abs(got - ref) / scale)))
+        checked += 1
+    assert checked > 20
+    assert worst < 1e-5, worst
+
+
+def _compare_runs(g: Planner, o: "kpo.Oracle", rg: dict, ro: dict):
+    for key in ("found", "best_cost", "best_leaf", "iterations", "propagations_attempted", "propagations_valid",
+                "nodes_committed", "nodes_pruned_terminal", "nodes_deactivated", "nodes_reactivated",
+                "candidates_dropped_capacity", "node_count", "capacity_exhausted", "first_solution_iteration",
+                "best_found_iteration", "timeline_len"):
+        assert rg[key] == ro[key], (key, rg[key], ro[key])
+    assert rg["propagations_admitted"] >= rg["nodes_committed"]
+    ng, no = g.nodes(), o.nodes()
+    for f in ("state", "control", "dt", "acc"):
+        np.testing.assert_array_equal(ng[f].astype(np.float64), no[f], err_msg=f)
+    np.testing.assert_array_equal(ng["parent"].astype(np.int64), no["parent"])
+    np.testing.assert_array_equal(ng["region"], no["region"])
+    np.testing.assert_array_equal(ng["status"], no["status"])
+    np.testing.assert_array_equal(ng["icount"].astype(np.uint32), np.minimum(no["icount"], 255))
+    tg = g.region_table().view(np.float32).astype(np.float64)
+    np.testing.assert_array_equal(tg, o.table())
+    lg, lo = g.timeline(), o.timeline()
+    assert [(e["iteration"], e["cost"], e["leaf"]) for e in lg] == [(e["iteration"], e["cost"], e["leaf"]) for e in lo]
+
+
+@pytest.mark.parametrize("scene,iters", [("forest_di6", 14), ("narrow_dubins6", 10), ("building_quad12", 6),
+                                          ("zigzag2d", 40), ("free2d", 30)])
+@pytest.mark.parametrize("rng_kind", ["philox", "splitmix"])
+def test_whole_run_bit_identical(scene, iters, rng_kind):
+    s = scenarios.load(scene, rng=rng_kind)
+    with Planner(s, seed=5) as g:
+        rg = g.solve(budget_s=0.0, max_iterations=iters)
+        o = kpo.Oracle(s, kpo.MIRROR32, seed=5, workers=8)
+        ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
+        _compare_runs(g, o, rg, ro)
+
+
+def test_whole_run_deactivate_and_capacity():
+    s = scenarios.load("forest_di6", deactivate_after_expansion=True, capacity=3000)
+    with Planner(s, seed=3) as g:
+        rg = g.solve(budget_s=0.0, max_iterations=12)
+        o = kpo.Oracle(s, kpo.MIRROR32, seed=3, workers=8)
+        ro = o.run(budget_s=0.0, max_iterations=12, stop_first=0)
+        assert rg["capacity_exhausted"] == 1
+        _compare_runs(g, o, rg, ro)
+
+
+def test_solve_continues_and_reset_repeats():
+    s = scenarios.load("forest_di6")
+    with Planner(s, seed=21) as g:
+        a = g.solve(budget_s=0.0, max_iterations=6)
+        b = g.solve(budget_s=0.0, max_iterations=6)
+        assert b["iterations"] == 12
+        g.reset(21)
+        c = g.solve(budget_s=0.0, max_iterations=12)
+        assert c["node_count"] == b["node_count"] and c["best_cost"] == b["best_cost"]
+        assert a["iterations"] == 6
