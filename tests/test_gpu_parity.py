@@ -20,12 +20,17 @@ SCENES = ["forest_di6", "narrow_dubins6", "building_quad12", "zigzag2d", "free2d
 
 
 def _random_parents(s, k, rng):
-    """Valid-ish parent states sampled inside the state bounds."""
+    """Valid parent states (the planner only ever expands stored, valid nodes;
+    samples[0] is not re-checked on the device), uniform in the state bounds."""
     lo = np.array([b[0] for b in s["problem"]["state_bounds"]], float)
     hi = np.array([b[1] for b in s["problem"]["state_bounds"]], float)
-    x = lo + (hi - lo) * rng.random((k, len(lo)))
-    x[0] = s["problem"]["x_init"]
-    return x.astype(np.float32)
+    o = kpo.Oracle(s, kpo.MIRROR32)
+    out = [np.asarray(s["problem"]["x_init"], np.float32)]
+    while len(out) < k:
+        x = (lo + (hi - lo) * rng.random(len(lo))).astype(np.float32)
+        if o.is_state_valid(x.astype(np.float64)):
+            out.append(x)
+    return np.stack(out)
 
 
 @pytest.mark.parametrize("scene", SCENES)
