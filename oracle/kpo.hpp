@@ -460,8 +460,11 @@ typename P::R pos_delta_norm(int m, const typename P::R* dlt) {
 }
 
 // is_segment_valid.  DECISION: between
-// consecutive samples a, b with ||b - a|| > c, k = ceil(d / c) and points
-// p_j = MADD(j/k, b - a, a), j = 1..k-1, are obstacle-checked.
+// consecutive samples a, b with d = ||b - a|| > c, k is the smallest power of
+// two with d / k <= c (dyadic, capped at 2^24) and the points
+// p_j = MADD(j/k, b - a, a), j = 1..k-1, are obstacle-checked.  Dyadic points
+// nest, so a finer collision_step re-checks every coarser point: the SPEC.md:231
+// monotone-refinement property holds exactly (ceil(d/c) points would not nest).
 template <class P>
 bool is_segment_valid(const ProblemDef& pd, const Consts<P>& k,
                       const std::vector<Vec<typename P::R>>& samples) {
@@ -477,7 +480,8 @@ bool is_segment_valid(const ProblemDef& pd, const Consts<P>& k,
         }
         const R d = pos_delta_norm<P>(w, dl);
         if (d > k.coll) {
-            const int kk = static_cast<int>(std::ceil(d / k.coll));
+            int kk = 2;
+            while (d / R(kk) > k.coll && kk < (1 << 24)) kk <<= 1;
             for (int jj = 1; jj < kk; ++jj) {
                 const R t = R(jj) / R(kk);
                 R p[3] = {0, 0, 0};

@@ -325,8 +325,9 @@ KP_DEV int propagate_item(const KpProblem& P, const float* __restrict__ sbox, co
         d2 = fmaf(dy, dy, d2);
         if (!TWO_D) d2 = fmaf(dz, dz, d2);
         const float d = sqrtf(d2);
-        if (d > P.coll) {
-            const int k = static_cast<int>(ceilf(d / P.coll));
+        if (d > P.coll) {  // dyadic subdivision (nested points)
+            int k = 2;
+            while (d / static_cast<float>(k) > P.coll && k < (1 << 24)) k <<= 1;
             for (int j = 1; j < k; ++j) {
                 const float t = static_cast<float>(j) / static_cast<float>(k);
                 o.points += 1;

@@ -170,7 +170,7 @@ def free2d() -> dict:
             "state_bounds": [[0, 10], [0, 10], [-1, 1], [-1, 1]],
             "control_bounds": [[-1, 1], [-1, 1]],
         },
-        "decomposition": {"dims": [0, 1], "cells": [20, 20]},
+        "decomposition": {"dims": [0, 1, 2, 3], "cells": [20, 20, 6, 6]},  # full state
         "planner": {
             "lambda": 8, "i_max": 5, "t_prop": 1.0, "capacity": 1 << 16, "ode_step": 0.05,
             "collision_step": 0.05, "t_max_ms": 100, "max_iterations": 0, "rng": "philox", "max_slots": 1 << 18,
@@ -200,7 +200,7 @@ def zigzag2d() -> dict:
             "state_bounds": [[0, 10], [0, 10], [-1.5, 1.5], [-1.5, 1.5]],
             "control_bounds": [[-1.5, 1.5], [-1.5, 1.5]],
         },
-        "decomposition": {"dims": [0, 1], "cells": [40, 40]},
+        "decomposition": {"dims": [0, 1, 2, 3], "cells": [40, 40, 6, 6]},  # full state
         "planner": {
             "lambda": 16, "i_max": 5, "t_prop": 0.8, "capacity": 1 << 18, "ode_step": 0.02,
             "collision_step": 0.05, "t_max_ms": 100, "max_iterations": 0, "rng": "philox", "max_slots": 1 << 20,
