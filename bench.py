@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Kino-PAX+ planning iteration (BASELINE.json).
+
+Metric: node propagations/sec (whole job), with the other two BASELINE metrics
+(ms to first solution, solution cost at 100 ms) reported in the same line.
+
+One step = one seeded query of the workload solved with a 100 ms budget
+(BASELINE "cost at 100 ms"): fresh tree/grid (Alg. 1 init), then iterations
+(propagate -> prune -> update) until the budget is spent.  Inputs (problem,
+obstacles) are resident in HBM; L2 is flushed (256 MiB write) before every
+step.  Timed with CUDA events on the planner's own stream; max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config forest_di6]
+  python bench.py --impl reference ...   # the reference CPU planner arm
+
+Multi-GPU (torchrun, one rank per GPU): replicas only — every rank solves its
+own seeds (seed = base + rank * K + i); no collective on the data path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def _peaks():
+    p = {"hbm_gbs": HBM_FALLBACK_GBS, "hbm_src": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
+    try:
+        m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        p["hbm_gbs"] = float(m["hbm_gbs"])
+        p["hbm_src"] = "measured (MEASURED_PEAKS.json)"
+        p["sm_max_mhz"] = float(m.get("sm_max_mhz", 1965.0))
+    except Exception:
+        pass
+    # FP32 issue peak: 148 SMs x 128 lanes x clock (one FP32 lane-op per lane per cycle);
+    # a measured FFMA-chain number is used when profiles/fp32_peak.json exists.
+    p["fp32_lane_ops"] = 148 * 128 * p["sm_max_mhz"] * 1e6
+    p["fp32_src"] = "nominal 148 SM x 128 lanes x sm_max_mhz"
+    try:
+        f = json.load(open(os.path.join(ROOT, "profiles", "fp32_peak.json")))
+        p["fp32_lane_ops"] = float(f["ffma_lane_ops_per_s"])
+        p["fp32_src"] = "measured FFMA chains (profiles/fp32_peak.json)"
+    except Exception:
+        pass
+    return p
+
+
+# Algorithmic FP32 lane-ops (FFMA/FADD/FMUL/FSETP/FMNMX/FDIV-as-1) of the
+# pinned recipe, per unit of device work counted by kp_profile.
+OPS_PER_STEP = {  # RK4 stages + combine + bounds/workspace compares + distance + cost add
+    "double_integrator_4d": 3 * 4 + 4 * 4 + 2 + (8 + 4) + 6 + 1,
+    "double_integrator_6d": 3 * 6 + 4 * 6 + 2 + (12 + 6) + 9 + 1,
+    "dubins_airplane_6d": 4 * (2 * 22 + 3) + 3 * 6 + 4 * 6 + 2 + 6 + (12 + 6) + 9 + 1,
+    "quadcopter_12d": 4 * (3 * 22 + 32) + 3 * 12 + 4 * 12 + 2 + 18 + (24 + 6) + 9 + 1,
+}
+OPS_PER_ITEM = 30      # sampling (4 fma + 4 cvt/mul), S = ceil(dt/h), region index, goal test, acc add
+OPS_PER_BOX = 6        # six closed-interval compares
+OPS_PER_SPHERE = 7     # 3 sub + mul + 2 fma + compare
+OPS_PER_INTERP = 4     # j/k + 3 fma
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for name, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(name)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _median(xs):
+    xs = [x for x in xs if x == x]
+    return statistics.median(xs) if xs else None
+
+
+def cpu_planner_run(scenario, seed, budget_s, workers, stop_first, max_iterations=0):
+    """The reference CPU planner (fp64 restatement, oracle/, SplitMix64, worker pool)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import kpo
+
+    s = json.loads(json.dumps(scenario))
+    s["planner"]["rng"] = "splitmix"  # rng.hpp derive_stream, as the reference
+    o = kpo.Oracle(s, kpo.FAITHFUL64, seed=seed, workers=workers)
+    t = time.perf_counter()
+    r = o.run(budget_s=budget_s, max_iterations=max_iterations, stop_first=1 if stop_first else 0)
+    r["wall_s"] = time.perf_counter() - t
+    return r
+
+
+def run_reference(args, scenario):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    budget = args.budget_ms / 1000.0
+    for i in range(args.warmup):
+        cpu_planner_run(scenario, args.seed_base - 1 - i, budget, cores, False)
+    props, wall, ttfs, costs, found = 0, 0.0, [], [], 0
+    for i in range(args.steps):
+        r = cpu_planner_run(scenario, args.seed_base + i, budget, cores, False)
+        props += r["propagations_attempted"]
+        wall += r["wall_s"]
+        if r["found"]:
+            found += 1
+            ttfs.append(r["first_solution_s"] * 1e3)
+            costs.append(r["best_cost"])
+    value = props / wall
+    line = {
+        "impl": "reference", "metric": "node propagations/sec", "value": value, "unit": "propagations/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "budget_ms": args.budget_ms, "seeds": [args.seed_base, args.seed_base + args.steps - 1]},
+        "metrics": {"ms_to_first_solution_median": _median(ttfs), "solution_cost_at_budget_median": _median(costs),
+                    "success_rate": found / args.steps, "node_propagations_per_sec": value},
+        "cpu_baseline": {"value": value, "unit": "propagations/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} queries x {args.budget_ms} ms budget, fp64 restatement "
+                                   f"(oracle/kpo.hpp Faithful64, SplitMix64), {cores} worker threads"},
+        "e2e": {"value": value, "unit": "propagations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_b200(args, scenario):
+    import torch
+
+    from paper_2602_02846_b200 import Planner
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    budget = args.budget_ms / 1000.0
+    planner = Planner(scenario, device=local, seed=args.seed_base)
+    ext = torch.cuda.ExternalStream(planner.stream(), device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    n = planner.n
+    x_init = scenario["problem"]["x_init"]
+    seeds = [args.seed_base + rank * args.steps + i for i in range(args.steps)]
+
+    for i in range(args.warmup):
+        planner.reset(args.seed_base + 100000 + i)
+        planner.solve(budget)
+
+    # ---- timed region (device) ----
+    prof0 = planner.profile()
+    results = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(ext)
+        for sd in seeds:
+            with torch.cuda.stream(ext):
+                flush.zero_()
+            planner.reset(sd)
+            results.append(planner.solve(budget))
+        e1.record(ext)
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    prof1 = planner.profile()
+    dev_ms = e0.elapsed_time(e1)
+    props = sum(r["propagations_attempted"] for r in results)
+    t = torch.tensor([dev_ms, float(props)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        mx = t.clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        sm = t.clone()
+        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+        dev_ms, props_total = float(mx[0]), float(sm[1])
+    else:
+        props_total = float(props)
+    value = props_total / (dev_ms / 1e3)
+
+    # ---- end-to-end through the public C-ABI with host buffers ----
+    e2e_props, t_e2e = 0, 0.0
+    d2h_path = 0
+    for sd in seeds:
+        t0 = time.perf_counter()
+        planner.reset(sd, x_init=x_init)          # H2D: start state (pinned staging), seed
+        r = planner.solve(budget)                  # D2H: result/control block
+        p = planner.path() if r["found"] else None  # D2H: root->leaf chain
+        t_e2e += time.perf_counter() - t0
+        e2e_props += r["propagations_attempted"]
+        if p is not None:
+            d2h_path += p["states"].nbytes // 2 + p["controls"].nbytes // 2 + 2 * 4 * len(p["durations"])
+    planner.set_stop_at_first_solution(True)
+    ttfs_wall = []
+    for sd in seeds:
+        t0 = time.perf_counter()
+        planner.reset(sd, x_init=x_init)
+        r = planner.solve(budget)
+        ttfs_wall.append((time.perf_counter() - t0) * 1e3 if r["found"] else float("nan"))
+    planner.set_stop_at_first_solution(False)
+    e = torch.tensor([t_e2e, float(e2e_props)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        emx = e.clone()
+        torch.distributed.all_reduce(emx, op=torch.distributed.ReduceOp.MAX)
+        esm = e.clone()
+        torch.distributed.all_reduce(esm, op=torch.distributed.ReduceOp.SUM)
+        t_e2e, e2e_total = float(emx[0]), float(esm[1])
+    else:
+        e2e_total = float(e2e_props)
+
+    # ---- per-kernel roofline pass (one query, per-launch CUDA events) ----
+    roof = None
+    if rank == 0:
+        planner.set_profiling(True)
+        pa = planner.profile()
+        planner.reset(seeds[0])
+        planner.solve(budget)
+        pb = planner.profile()
+        planner.set_profiling(False)
+        roof = roofline(scenario, pa, pb)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        r = cpu_planner_run(scenario, seeds[0], args.cpu_budget_s, cores, True)
+        cpu = {"value": r["propagations_attempted"] / r["wall_s"], "unit": "propagations/s", "cores": cores,
+               "kind": "port",
+               "sample": f"{args.config} seed {seeds[0]}, one query run to its first solution "
+                         f"(cap {args.cpu_budget_s:.0f} s), fp64 restatement (oracle Faithful64, SplitMix64)",
+               "ms_to_first_solution": r["first_solution_s"] * 1e3 if r["found"] else None,
+               "first_solution_cost": r["best_cost"] if r["found"] else None,
+               "iterations": r["iterations"]}
+
+    if rank == 0:
+        ttfs = [r["first_solution_s"] * 1e3 for r in results if r["found"]]
+        costs = [r["best_cost"] for r in results if r["found"]]
+        launches = prof1["kernel_launches"] - prof0["kernel_launches"] + 2 * len(seeds)
+        ctl_bytes = 98_688
+        line = {
+            "metric": "node propagations/sec", "value": value, "unit": "propagations/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / len(seeds),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (pinned scene geometry, seeded queries)",
+            "config": {"workload": f"{args.config}: one seeded query per step, {args.budget_ms:g} ms budget "
+                                   "(Alg. 1 until t_max), replicas across ranks",
+                       "budget_ms": args.budget_ms, "seeds_rank0": [seeds[0], seeds[-1]],
+                       "lambda": scenario["planner"]["lambda"], "capacity": scenario["planner"]["capacity"],
+                       "regions": _regions(scenario), "l2": "flushed before every step (256 MiB write)",
+                       "parallelism": f"replicas x{ws}"},
+            "metrics": {
+                "ms_to_first_solution_median": _median(ttfs),
+                "ms_to_first_solution_p25_p75": _quart(ttfs),
+                "solution_cost_at_100ms_median": _median(costs) if abs(args.budget_ms - 100) < 1e-9 else None,
+                "solution_cost_at_budget_median": _median(costs),
+                "success_rate": len(ttfs) / len(results),
+                "node_propagations_per_sec": value,
+                "iterations_median": _median([r["iterations"] for r in results]),
+                "capacity_exhausted_steps": sum(r["capacity_exhausted"] for r in results),
+            },
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_total / t_e2e, "unit": "propagations/s",
+                    "h2d_bytes_per_step": 4 * 12 + 8,
+                    "d2h_bytes_per_step": int(ctl_bytes + d2h_path / max(1, len(seeds))),
+                    "ms_to_first_solution_median_wall": _median(ttfs_wall),
+                    "note": "host wall clock around kp_reset_query + kp_solve + kp_get_path per query"},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    planner.close()
+    return 0
+
+
+def _quart(xs):
+    xs = sorted(x for x in xs if x == x)
+    if len(xs) < 2:
+        return None
+    return [xs[len(xs) // 4], xs[(3 * len(xs)) // 4]]
+
+
+def _regions(s):
+    r = 1
+    for c in s["decomposition"].get("cells", []):
+        r *= c
+    return r
+
+
+def roofline(scenario, pa, pb):
+    """Dominant kernel = propagate (FP32 issue-bound, no tensor-core work);
+    select/scatter reported against HBM bandwidth."""
+    pk = _peaks()
+    model = scenario["problem"]["model"]
+    d = {k: pb[k] - pa[k] for k in pb}
+    ops = (d["rk4_steps"] * OPS_PER_STEP[model] + d["items"] * OPS_PER_ITEM + d["box_tests"] * OPS_PER_BOX
+           + d["sphere_tests"] * OPS_PER_SPHERE + d["interp_points"] * OPS_PER_INTERP)
+    n_prop = max(1, d["n_propagate"])
+    t_prop = d["t_propagate_s"] / n_prop
+    ops_launch = ops / n_prop
+    achieved = ops_launch / t_prop if t_prop > 0 else 0.0
+    n = {"double_integrator_4d": 4, "double_integrator_6d": 6, "dubins_airplane_6d": 6, "quadcopter_12d": 12}[model]
+    m = {"double_integrator_4d": 2, "double_integrator_6d": 3, "dubins_airplane_6d": 3, "quadcopter_12d": 4}[model]
+    # select + scatter algorithmic bytes: live node prune, ancestor hops, slot scan, commits
+    sel_bytes = (d["live_scanned"] * 15 + d["ancestor_hops"] * 16 + d["slots_scanned"] / 8 * 3
+                 + d["admitted_checked"] * 12)
+    n_sel = max(1, d["n_select"])
+    t_sel = d["t_select_s"] / n_sel
+    sel_gbs = sel_bytes / n_sel / t_sel / 1e9 if t_sel > 0 else 0.0
+    t_total = d["t_propagate_s"] + d["t_select_s"] + d["t_scatter_s"]
+    return {
+        "kernel": "k_propagate",
+        "bound": "fp32",
+        "achieved": achieved / 1e12, "peak": pk["fp32_lane_ops"] / 1e12, "unit": "T lane-op/s",
+        "frac": achieved / pk["fp32_lane_ops"], "traffic": None,
+        "peak_src": pk["fp32_src"],
+        "ops_per_launch": ops_launch, "avg_launch_us": t_prop * 1e6, "launches": n_prop,
+        "ops_convention": "FP32 lane-ops of the pinned recipe: FFMA, FADD, FMUL, FSETP, FMNMX, FDIV each = 1",
+        "share_of_iteration_time": d["t_propagate_s"] / t_total if t_total else None,
+        "select": {"kernel": "k_select_reduce", "bound": "hbm", "achieved": sel_gbs, "peak": pk["hbm_gbs"],
+                   "unit": "GB/s", "frac": sel_gbs / pk["hbm_gbs"], "avg_launch_us": t_sel * 1e6,
+                   "peak_src": pk["hbm_src"],
+                   "share_of_iteration_time": d["t_select_s"] / t_total if t_total else None},
+        "scatter": {"kernel": "k_select_scatter", "avg_launch_us": d["t_scatter_s"] / max(1, d["n_scatter"]) * 1e6,
+                    "share_of_iteration_time": d["t_scatter_s"] / t_total if t_total else None},
+        "state_dims": n, "control_dims": m,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="forest_di6",
+                    choices=["forest_di6", "narrow_dubins6", "building_quad12", "zigzag2d", "free2d"])
+    ap.add_argument("--budget-ms", type=float, default=100.0)
+    ap.add_argument("--seed-base", type=int, default=1000)
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_2602_02846_b200 import scenarios
+
+    scenario = scenarios.load(args.config)
+    if args.impl == "reference":
+        return run_reference(args, scenario)
+    return run_b200(args, scenario)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

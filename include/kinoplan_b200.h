@@ -174,6 +174,15 @@ const char* kp_last_error(const kp_planner* planner);
  * ("trial k uses seed = base_seed + k"). */
 int kp_reset(kp_planner* planner, uint64_t seed);
 
+/* One query = (seed, start state).  Like kp_reset, but also replaces x_init
+ * with the host array x_init[state_dim] (copied host->device; NULL keeps the
+ * current start).  The new start is validated (InvalidProblemError,
+ * SPEC.md:61, :374). */
+int kp_reset_query(kp_planner* planner, uint64_t seed, const double* x_init);
+
+/* Toggle PlannerConfig.stop_at_first_solution for later kp_solve calls. */
+int kp_set_stop_at_first_solution(kp_planner* planner, int enabled);
+
 /* ---- solve -------------------------------------------------------------- */
 
 /* Replaces plan(problem, config).  Runs Alg. 1 iterations
@@ -233,11 +242,33 @@ int kp_debug_propagate(kp_planner* planner, size_t n, const float* parent_states
                        float* final_states, float* controls, float* durations, float* acc,
                        uint32_t* region, uint32_t* steps, uint8_t* in_goal);
 
-/* Device time spent in each kernel class during the last kp_solve, in seconds
- * (CUDA events bracketing each launch; only when profiling was enabled with
- * kp_set_profiling).  out[0] propagate, out[1] select, out[2] scatter. */
+/* Work and timing counters for roofline accounting (bench.py).  Device
+ * counters are cumulative since the last kp_reset; kernel_launches /
+ * graph_launches since kp_create; the per-class CUDA-event times are only
+ * collected while profiling is on (kp_set_profiling), one launch at a time. */
+typedef struct kp_profile {
+    uint64_t kernel_launches;   /* kernels enqueued by the library (graph nodes counted individually) */
+    uint64_t graph_launches;
+    double t_propagate_s, t_select_s, t_scatter_s;
+    uint64_t n_propagate, n_select, n_scatter;
+    uint64_t items;             /* propagate work items (== propagations_attempted) */
+    uint64_t rk4_steps;         /* RK4 steps executed (valid + invalid items) */
+    uint64_t samples_checked;   /* integration samples validity-checked */
+    uint64_t interp_points;     /* interpolated points obstacle-checked */
+    uint64_t box_tests;         /* point-vs-box tests executed */
+    uint64_t sphere_tests;      /* point-vs-sphere tests executed */
+    uint64_t live_scanned;      /* live nodes visited by the prune pass */
+    uint64_t ancestor_hops;     /* parent hops of the ancestor-domination walks */
+    uint64_t slots_scanned;     /* V_U slots visited by select */
+    uint64_t admitted_checked;  /* admitted slots commit-tested */
+} kp_profile;
+
 int kp_set_profiling(kp_planner* planner, int enabled);
-int kp_get_kernel_times(kp_planner* planner, double* out3, uint64_t* launches3);
+int kp_get_profile(kp_planner* planner, kp_profile* out);
+
+/* The CUDA stream (cudaStream_t) every kernel of this handle is launched on,
+ * so a caller can bracket work with its own CUDA events. */
+int kp_get_stream(kp_planner* planner, void** stream);
 
 /* ---- batched independent queries (BASELINE config 4) -------- */
 

@@ -123,6 +123,18 @@ class Result(C.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class Profile(C.Structure):
+    _fields_ = [("kernel_launches", C.c_uint64), ("graph_launches", C.c_uint64), ("t_propagate_s", C.c_double),
+                ("t_select_s", C.c_double), ("t_scatter_s", C.c_double), ("n_propagate", C.c_uint64),
+                ("n_select", C.c_uint64), ("n_scatter", C.c_uint64), ("items", C.c_uint64),
+                ("rk4_steps", C.c_uint64), ("samples_checked", C.c_uint64), ("interp_points", C.c_uint64),
+                ("box_tests", C.c_uint64), ("sphere_tests", C.c_uint64), ("live_scanned", C.c_uint64),
+                ("ancestor_hops", C.c_uint64), ("slots_scanned", C.c_uint64), ("admitted_checked", C.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 class TimelineEntry(C.Structure):
     _fields_ = [("iteration", C.c_uint64), ("elapsed_s", C.c_double), ("cost", C.c_double), ("leaf", C.c_int64)]
 
@@ -267,6 +279,10 @@ def load_library() -> C.CDLL:
     L.kp_last_error.restype = C.c_char_p
     L.kp_reset.argtypes = [P, C.c_uint64]
     L.kp_reset.restype = I
+    L.kp_reset_query.argtypes = [P, C.c_uint64, P]
+    L.kp_reset_query.restype = I
+    L.kp_set_stop_at_first_solution.argtypes = [P, I]
+    L.kp_set_stop_at_first_solution.restype = I
     L.kp_solve.argtypes = [P, D, C.c_uint64, CP(Result)]
     L.kp_solve.restype = I
     L.kp_solve_batch.argtypes = [P, CP(C.c_uint64), C.c_size_t, D, C.c_uint64, CP(Result)]
@@ -287,8 +303,10 @@ def load_library() -> C.CDLL:
     L.kp_debug_propagate.restype = I
     L.kp_set_profiling.argtypes = [P, I]
     L.kp_set_profiling.restype = I
-    L.kp_get_kernel_times.argtypes = [P, CP(D), CP(C.c_uint64)]
-    L.kp_get_kernel_times.restype = I
+    L.kp_get_profile.argtypes = [P, CP(Profile)]
+    L.kp_get_profile.restype = I
+    L.kp_get_stream.argtypes = [P, CP(C.c_void_p)]
+    L.kp_get_stream.restype = I
     L.kp_abi_version.argtypes = []
     L.kp_abi_version.restype = I
     _LIB = L
@@ -296,9 +314,10 @@ def load_library() -> C.CDLL:
 
 
 EXPORTED_SYMBOLS = [
-    "kp_create", "kp_destroy", "kp_last_error", "kp_reset", "kp_solve", "kp_get_timeline", "kp_get_path",
+    "kp_create", "kp_destroy", "kp_last_error", "kp_reset", "kp_reset_query", "kp_set_stop_at_first_solution",
+    "kp_solve", "kp_get_timeline", "kp_get_path",
     "kp_get_trajectory", "kp_get_nodes", "kp_get_region_table", "kp_get_grid", "kp_debug_propagate",
-    "kp_set_profiling", "kp_get_kernel_times", "kp_solve_batch", "kp_abi_version",
+    "kp_set_profiling", "kp_get_profile", "kp_get_stream", "kp_solve_batch", "kp_abi_version",
 ]
 
 

@@ -83,6 +83,9 @@ struct kp_planner {
     uint64_t klaunch[3] = {0, 0, 0};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     uint64_t seed = 0;
+    uint64_t kernel_launches = 0, graph_launches = 0;
+    std::vector<float> boxes, spheres;  // host copies for start-state validation
+    float* h_x0 = nullptr;              // pinned staging for the query's start state
 
     template <class T>
     T* dalloc(size_t count) {
@@ -98,6 +101,7 @@ struct kp_planner {
             if (e) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
         if (host_done) cudaFreeHost(host_done);
+        if (h_x0) cudaFreeHost(h_x0);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -313,7 +317,10 @@ void capture_graph(kp_planner* pl) {
 
 void do_reset(kp_planner* pl, uint64_t seed) {
     pl->seed = seed;
+    cuda_check(cudaMemcpyAsync(pl->B.x0, pl->h_x0, sizeof(float) * KP_MAX_N, cudaMemcpyHostToDevice, pl->stream),
+               "x0 H2D");
     cuda_check(kp::launch_reset(pl->P, pl->B, seed, pl->stream), "reset");
+    pl->kernel_launches += 2;
     cuda_check(cudaStreamSynchronize(pl->stream), "reset sync");
     pl->ctl_valid = false;
 }
@@ -477,6 +484,13 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         B.boxes = db;
         B.spheres = ds;
         B.ctl = pl->dalloc<KpCtl>(1);
+        B.x0 = pl->dalloc<float>(KP_MAX_N);
+        void* hx = nullptr;
+        cuda_check(cudaHostAlloc(&hx, sizeof(float) * KP_MAX_N, cudaHostAllocDefault), "cudaHostAlloc x0");
+        pl->h_x0 = static_cast<float*>(hx);
+        for (int i = 0; i < KP_MAX_N; ++i) pl->h_x0[i] = i < P.n ? P.x_init[i] : 0.0f;
+        pl->boxes = boxes;
+        pl->spheres = spheres;
         cuda_check(kp::set_propagate_smem(P), "smem attribute");
         const int occ = std::max(1, kp::propagate_occupancy(P));
         pl->grid_prop = pl->sms * occ;
@@ -503,18 +517,64 @@ int kp_reset(kp_planner* pl, uint64_t seed) {
     });
 }
 
+int kp_reset_query(kp_planner* pl, uint64_t seed, const double* x_init) {
+    if (!pl) return KP_ERR_ARGUMENT;
+    return guard(pl, [&] {
+        cuda_check(cudaSetDevice(pl->device), "cudaSetDevice");
+        if (x_init) {
+            KpProblem q = pl->P;
+            for (int i = 0; i < pl->P.n; ++i) q.x_init[i] = static_cast<float>(x_init[i]);
+            if (!host_state_valid(q, pl->boxes, pl->spheres))
+                throw KpError(KP_ERR_INVALID_PROBLEM, "x_init is not a valid state (SPEC.md:61, :374)");
+            for (int i = 0; i < pl->P.n; ++i) pl->h_x0[i] = q.x_init[i];
+            pl->P.x_init[0] = pl->P.x_init[0];  // P itself is unchanged (captured graph args)
+        }
+        do_reset(pl, seed);
+    });
+}
+
+int kp_set_stop_at_first_solution(kp_planner* pl, int enabled) {
+    if (!pl) return KP_ERR_ARGUMENT;
+    pl->cfg.stop_at_first_solution = enabled ? 1 : 0;
+    return KP_OK;
+}
+
 int kp_set_profiling(kp_planner* pl, int enabled) {
     if (!pl) return KP_ERR_ARGUMENT;
     pl->profiling = enabled != 0;
     return KP_OK;
 }
 
-int kp_get_kernel_times(kp_planner* pl, double* out3, uint64_t* launches3) {
-    if (!pl || !out3) return KP_ERR_ARGUMENT;
-    for (int i = 0; i < 3; ++i) {
-        out3[i] = pl->ktime[i];
-        if (launches3) launches3[i] = pl->klaunch[i];
-    }
+int kp_get_profile(kp_planner* pl, kp_profile* out) {
+    if (!pl || !out) return KP_ERR_ARGUMENT;
+    return guard(pl, [&] {
+        fetch_ctl(pl);
+        const KpStats& st = pl->ctl.stats;
+        std::memset(out, 0, sizeof *out);
+        out->kernel_launches = pl->kernel_launches;
+        out->graph_launches = pl->graph_launches;
+        out->t_propagate_s = pl->ktime[0];
+        out->t_select_s = pl->ktime[1];
+        out->t_scatter_s = pl->ktime[2];
+        out->n_propagate = pl->klaunch[0];
+        out->n_select = pl->klaunch[1];
+        out->n_scatter = pl->klaunch[2];
+        out->items = st.attempted;
+        out->rk4_steps = st.rk4_steps;
+        out->samples_checked = st.rk4_steps;  // every executed step's sample is validity-checked
+        out->interp_points = st.interp_points;
+        out->box_tests = st.box_tests;
+        out->sphere_tests = st.sphere_tests;
+        out->live_scanned = st.live_scanned;
+        out->ancestor_hops = st.ancestor_hops;
+        out->slots_scanned = st.slots_scanned;
+        out->admitted_checked = st.admitted_checked;
+    });
+}
+
+int kp_get_stream(kp_planner* pl, void** stream) {
+    if (!pl || !stream) return KP_ERR_ARGUMENT;
+    *stream = static_cast<void*>(pl->stream);
     return KP_OK;
 }
 
@@ -532,6 +592,7 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
         *pl->host_done = 0;
         cuda_check(kp::launch_start(pl->B, budget_ns, static_cast<uint32_t>(mi), stop_first ? 1u : 0u, pl->stream),
                    "start");
+        pl->kernel_launches += 1;
         // host watchdog: the device stops itself at the budget; this only
         // guards against a hang (budget + 60 s, or 600 s for iteration-only runs).
         const double watchdog = (budget > 0 ? budget : 540.0) + 60.0;
@@ -544,6 +605,7 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
                 for (int k = 0; k < 3; ++k) {
                     cuda_check(cudaEventRecord(pl->ev[0], pl->stream), "event");
                     cuda_check(kp::launch_iteration(pl->P, pl->B, pl->grid_prop, pl->grid_sel, pl->stream, 1 << k), "iter");
+                    pl->kernel_launches += 1;
                     cuda_check(cudaEventRecord(pl->ev[1], pl->stream), "event");
                     cuda_check(cudaEventSynchronize(pl->ev[1]), "event sync");
                     float ms = 0;
@@ -571,6 +633,8 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
                     if (*done) break;
                 }
                 cuda_check(cudaGraphLaunch(pl->graph, pl->stream), "cudaGraphLaunch");
+                pl->graph_launches += 1;
+                pl->kernel_launches += 3 * KP_GRAPH_ITERS;
                 cuda_check(cudaEventRecord(inflight[n_launched & 1], pl->stream), "event");
                 ++n_launched;
             }

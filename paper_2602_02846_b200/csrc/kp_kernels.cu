@@ -57,10 +57,10 @@ __global__ void __launch_bounds__(256) k_propagate(KpProblem P, KpBuffers B) {
     extern __shared__ float smem[];
     float* sbox = smem;
     float* ssph = smem + 6 * P.n_box;
-    __shared__ unsigned long long s_cnt[4];
+    __shared__ unsigned long long s_cnt[6];
     KpCtl* ctl = B.ctl;
     if (ctl->done) return;
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 6) s_cnt[threadIdx.x] = 0;
     stage_obstacles(P, B, sbox, ssph);
     const uint32_t n_items = ctl->n_items;
     const uint32_t it = ctl->iter;
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) k_propagate(KpProblem P, KpBuffers B) {
     const uint32_t padded = (n_items + 31u) & ~31u;
     const uint32_t cap = P.capacity, S = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
-    uint32_t n_valid = 0, n_adm = 0, n_steps = 0, n_pts = 0;
+    uint32_t c[6] = {0, 0, 0, 0, 0, 0};  // valid, admitted, steps, interp, box tests, sphere tests
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < padded; i += gridDim.x * blockDim.x) {
         bool adm = false, goal = false;
         if (i < n_items) {
@@ -82,15 +82,17 @@ __global__ void __launch_bounds__(256) k_propagate(KpProblem P, KpBuffers B) {
             const float acc_p = __uint_as_float(B.acc[node]);
             ItemOut o;
             const int rc = propagate_item<MODEL>(P, sbox, ssph, x, acc_p, seed, it, node, br, u, dt, o);
-            n_steps += o.steps;
-            n_pts += o.points;
+            c[2] += o.steps;
+            c[3] += o.interp;
+            c[4] += o.nbox;
+            c[5] += o.nsph;
             if (rc == 0) {
-                ++n_valid;
+                ++c[0];
                 const uint32_t bits = __float_as_uint(o.acc);
                 const uint32_t old = atomicMin(B.rc + o.region, bits);
                 adm = bits <= old;  // Improved or Equal
                 if (adm) {
-                    ++n_adm;
+                    ++c[1];
                     goal = o.goal;
 #pragma unroll
                     for (int d = 0; d < N; ++d) B.vu_state[static_cast<size_t>(d) * S + i] = x[d];
@@ -111,24 +113,23 @@ __global__ void __launch_bounds__(256) k_propagate(KpProblem P, KpBuffers B) {
     }
     // warp-aggregated then block-aggregated counters
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        n_valid += __shfl_down_sync(0xFFFFFFFFu, n_valid, off);
-        n_adm += __shfl_down_sync(0xFFFFFFFFu, n_adm, off);
-        n_steps += __shfl_down_sync(0xFFFFFFFFu, n_steps, off);
-        n_pts += __shfl_down_sync(0xFFFFFFFFu, n_pts, off);
+    for (int k = 0; k < 6; ++k) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) c[k] += __shfl_down_sync(0xFFFFFFFFu, c[k], off);
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&s_cnt[0], static_cast<unsigned long long>(n_valid));
-        atomicAdd(&s_cnt[1], static_cast<unsigned long long>(n_adm));
-        atomicAdd(&s_cnt[2], static_cast<unsigned long long>(n_steps));
-        atomicAdd(&s_cnt[3], static_cast<unsigned long long>(n_pts));
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (c[k]) atomicAdd(&s_cnt[k], static_cast<unsigned long long>(c[k]));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_cnt[0]) atomicAdd(&ctl->stats.valid, s_cnt[0]);
         if (s_cnt[1]) atomicAdd(&ctl->stats.admitted, s_cnt[1]);
         if (s_cnt[2]) atomicAdd(&ctl->stats.rk4_steps, s_cnt[2]);
-        if (s_cnt[3]) atomicAdd(&ctl->stats.points_checked, s_cnt[3]);
+        if (s_cnt[3]) atomicAdd(&ctl->stats.interp_points, s_cnt[3]);
+        if (s_cnt[4]) atomicAdd(&ctl->stats.box_tests, s_cnt[4]);
+        if (s_cnt[5]) atomicAdd(&ctl->stats.sphere_tests, s_cnt[5]);
     }
 }
 
@@ -174,7 +175,7 @@ KP_DEV Cnt3 block_scan3(Cnt3 x, Cnt3* total) {
 // prune_pass rules for one live node (priorities :434-437).
 // Returns the new status; writes status / i_count when they change.
 KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, uint32_t* term, uint32_t* deact,
-                          uint32_t* react) {
+                          uint32_t* react, uint32_t* hops) {
     const uint8_t st = B.status[g];
     const uint32_t a = B.acc[g];
     if (a > B.rc[B.region[g]]) {  // (1) dominated -> Terminal (absorbing)
@@ -197,6 +198,7 @@ KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, ui
     bool dominated = P.deact != 0;
     int32_t p = B.parent[g];
     while (!dominated && p >= 0) {
+        ++*hops;
         if (B.acc[p] > B.rc[B.region[p]]) dominated = true;
         p = B.parent[p];
     }
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
     KpCtl* ctl = B.ctl;
     if (ctl->done) return;
     __shared__ unsigned int s_last;
-    __shared__ uint32_t s_st[3];
+    __shared__ uint32_t s_st[7];
     const uint32_t it = ctl->iter;
     const uint32_t n_live = ctl->n_live;
     const uint32_t live_pad = (n_live + 31u) & ~31u;
@@ -221,20 +223,23 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
     const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
     const uint32_t n_tiles = (E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
     const uint32_t* __restrict__ live = B.live[it & 1];
-    uint32_t term = 0, deact = 0, react = 0;
-    if (threadIdx.x < 3) s_st[threadIdx.x] = 0;
+    uint32_t term = 0, deact = 0, react = 0, hops = 0, nlive = 0, nslot = 0, nadm = 0;
+    if (threadIdx.x < 7) s_st[threadIdx.x] = 0;
     __syncthreads();
     for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
         Cnt3 x{0, 0, 0};
         bool commit = false;
         if (e < n_live) {
-            const uint8_t st = prune_node(P, B, live[e], &term, &deact, &react);
+            ++nlive;
+            const uint8_t st = prune_node(P, B, live[e], &term, &deact, &react, &hops);
             x.k = st != KP_ST_TERMINAL;
             x.v = st == KP_ST_ACTIVE;
         } else if (e >= live_pad && e < E) {
             const uint32_t s = e - live_pad;
+            nslot += s < n_items;
             if (s < n_items && ((B.admit_mask[s >> 5] >> (s & 31)) & 1u)) {
+                ++nadm;
                 commit = B.vu_acc[s] == B.rc[B.vu_region[s]];  // Alg. 4 line 3, bit-exact
                 x.c = commit;
             }
@@ -253,12 +258,20 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
     if (term) atomicAdd(&s_st[0], term);
     if (deact) atomicAdd(&s_st[1], deact);
     if (react) atomicAdd(&s_st[2], react);
+    if (hops) atomicAdd(&s_st[3], hops);
+    if (nlive) atomicAdd(&s_st[4], nlive);
+    if (nslot) atomicAdd(&s_st[5], nslot);
+    if (nadm) atomicAdd(&s_st[6], nadm);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_st[0]) atomicAdd(&ctl->stats.pruned_terminal, static_cast<unsigned long long>(s_st[0]));
         if (s_st[1]) atomicAdd(&ctl->stats.deactivated, static_cast<unsigned long long>(s_st[1]));
         if (s_st[2]) atomicAdd(&ctl->stats.reactivated, static_cast<unsigned long long>(s_st[2]));
+        if (s_st[3]) atomicAdd(&ctl->stats.ancestor_hops, static_cast<unsigned long long>(s_st[3]));
+        if (s_st[4]) atomicAdd(&ctl->stats.live_scanned, static_cast<unsigned long long>(s_st[4]));
+        if (s_st[5]) atomicAdd(&ctl->stats.slots_scanned, static_cast<unsigned long long>(s_st[5]));
+        if (s_st[6]) atomicAdd(&ctl->stats.admitted_checked, static_cast<unsigned long long>(s_st[6]));
         __threadfence();
         s_last = (atomicAdd(&ctl->ticket_a, 1u) == gridDim.x - 1);
     }
@@ -435,7 +448,7 @@ __global__ void k_reset_root(KpProblem P, KpBuffers B, unsigned long long seed) 
     ctl->seed = seed;
     float x[KP_MAX_N];
     for (int d = 0; d < P.n; ++d) {
-        x[d] = P.x_init[d];
+        x[d] = B.x0[d];
         B.state[static_cast<size_t>(d) * P.capacity] = x[d];
     }
     for (int d = 0; d < P.m; ++d) B.ctrl[static_cast<size_t>(d) * P.capacity] = 0.0f;

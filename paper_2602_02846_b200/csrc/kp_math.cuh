@@ -208,22 +208,32 @@ KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk) {
 }
 
 // --------------------------------------------------------- environment ----
-// Position outside every closed obstacle?  Obstacles staged in shared memory;
-// every lane reads the same primitive at the same time (broadcast).
+// Position inside some closed obstacle?  Obstacles staged in shared memory;
+// every lane reads the same primitive at the same time (broadcast).  `tests`
+// accumulates the primitive tests executed (roofline accounting; boxes in
+// the low 32 bits' role via two counters).
 KP_DEV bool in_obstacle(const float* __restrict__ sbox, int n_box, const float* __restrict__ ssph, int n_sph,
-                        float px, float py, float pz) {
+                        float px, float py, float pz, uint32_t& nbox, uint32_t& nsph) {
     for (int b = 0; b < n_box; ++b) {
         const float* o = sbox + 6 * b;
-        if (px >= o[0] && px <= o[3] && py >= o[1] && py <= o[4] && pz >= o[2] && pz <= o[5]) return true;
+        if (px >= o[0] && px <= o[3] && py >= o[1] && py <= o[4] && pz >= o[2] && pz <= o[5]) {
+            nbox += b + 1;
+            return true;
+        }
     }
+    nbox += n_box;
     for (int s = 0; s < n_sph; ++s) {
         const float* o = ssph + 4 * s;
         const float dx = px - o[0], dy = py - o[1], dz = pz - o[2];
         float d2 = dx * dx;
         d2 = fmaf(dy, dy, d2);
         d2 = fmaf(dz, dz, d2);
-        if (d2 <= o[3]) return true;
+        if (d2 <= o[3]) {
+            nsph += s + 1;
+            return true;
+        }
     }
+    nsph += n_sph;
     return false;
 }
 
@@ -286,8 +296,9 @@ KP_DEV bool in_goal(const KpProblem& P, const float* x) {
 struct ItemOut {
     float acc;
     uint32_t region;
-    uint32_t steps;
-    uint32_t points;
+    uint32_t steps;    // RK4 steps executed
+    uint32_t interp;   // interpolated points checked
+    uint32_t nbox, nsph;  // primitive tests executed
     bool goal;
 };
 
@@ -310,16 +321,17 @@ KP_DEV int propagate_item(const KpProblem& P, const float* __restrict__ sbox, co
     float px = x[0], py = x[1], pz = TWO_D ? 0.0f : x[2];
     float total = 0.0f;
     o.steps = 0;
-    o.points = 0;
+    o.interp = 0;
+    o.nbox = 0;
+    o.nsph = 0;
     for (int s = 0; s < S; ++s) {
         const float hk = (s + 1 < S) ? P.h : dt - static_cast<float>(S - 1) * P.h;
         if (!(hk > 0.0f)) break;
         if (!rk4_step<MODEL>(P, x, u, hk)) return 2;
         o.steps += 1;
         const float nx = x[0], ny = x[1], nz = TWO_D ? 0.0f : x[2];
-        o.points += 1;
         if (!within_bounds<MODEL>(P, x)) return 1;
-        if (in_obstacle(sbox, P.n_box, ssph, P.n_sph, nx, ny, nz)) return 1;
+        if (in_obstacle(sbox, P.n_box, ssph, P.n_sph, nx, ny, nz, o.nbox, o.nsph)) return 1;
         const float dx = nx - px, dy = ny - py, dz = nz - pz;
         float d2 = dx * dx;
         d2 = fmaf(dy, dy, d2);
@@ -330,9 +342,9 @@ KP_DEV int propagate_item(const KpProblem& P, const float* __restrict__ sbox, co
             while (d / static_cast<float>(k) > P.coll && k < (1 << 24)) k <<= 1;
             for (int j = 1; j < k; ++j) {
                 const float t = static_cast<float>(j) / static_cast<float>(k);
-                o.points += 1;
+                o.interp += 1;
                 if (in_obstacle(sbox, P.n_box, ssph, P.n_sph, fmaf(t, dx, px), fmaf(t, dy, py),
-                                TWO_D ? 0.0f : fmaf(t, dz, pz)))
+                                TWO_D ? 0.0f : fmaf(t, dz, pz), o.nbox, o.nsph))
                     return 1;
             }
         }

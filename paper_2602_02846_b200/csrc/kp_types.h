@@ -57,7 +57,9 @@ struct KpProblem {
 struct KpStats {
     unsigned long long attempted, valid, admitted, committed;
     unsigned long long pruned_terminal, deactivated, reactivated, dropped_capacity;
-    unsigned long long rk4_steps, points_checked;  // roofline accounting (valid + invalid items)
+    // roofline accounting (valid + invalid items)
+    unsigned long long rk4_steps, samples_checked, interp_points, box_tests, sphere_tests;
+    unsigned long long live_scanned, ancestor_hops, slots_scanned, admitted_checked;
 };
 
 struct KpTimeline {
@@ -122,6 +124,7 @@ struct KpBuffers {
     // obstacles: boxes [n_box][6] (lo xyz, hi xyz), spheres [n_sph][4] (c xyz, r^2)
     const float* boxes;
     const float* spheres;
+    float* x0;              // [KP_MAX_N] current query's start state (H2D per query)
     KpCtl* ctl;
     volatile uint32_t* host_done;  // mapped pinned word (device writes 1 at termination)
 };

@@ -95,8 +95,16 @@ class Planner:
         if rc:
             _raise(rc, self._lib.kp_last_error(self._h))
 
-    def reset(self, seed: int):
-        self._check(self._lib.kp_reset(self._h, seed))
+    def reset(self, seed: int, x_init=None):
+        """New query: seed and (optionally) a new start state, copied host->device."""
+        if x_init is None:
+            self._check(self._lib.kp_reset(self._h, seed))
+        else:
+            self._x0 = np.ascontiguousarray(x_init, np.float64)
+            self._check(self._lib.kp_reset_query(self._h, seed, ptr(self._x0)))
+
+    def set_stop_at_first_solution(self, on: bool):
+        self._check(self._lib.kp_set_stop_at_first_solution(self._h, 1 if on else 0))
 
     # -- solve -------------------------------------------------------------
     def solve(self, budget_s: float = -1.0, max_iterations: int = 0) -> dict:
@@ -188,11 +196,15 @@ class Planner:
     def set_profiling(self, on: bool):
         self._check(self._lib.kp_set_profiling(self._h, 1 if on else 0))
 
-    def kernel_times(self):
-        t = (C.c_double * 3)()
-        n = (C.c_uint64 * 3)()
-        self._check(self._lib.kp_get_kernel_times(self._h, t, n))
-        return list(t), list(n)
+    def profile(self) -> dict:
+        pr = _capi.Profile()
+        self._check(self._lib.kp_get_profile(self._h, C.byref(pr)))
+        return pr.as_dict()
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        self._check(self._lib.kp_get_stream(self._h, C.byref(s)))
+        return s.value or 0
 
 
 def plan(scenario: dict, seed: int | None = None, device: int = 0, budget_s: float = -1.0,
