@@ -193,6 +193,9 @@ def run_b200(args, scenario):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     budget = args.budget_ms / 1000.0
+    iters = args.iters
+    if iters > 0:
+        budget = 0.0
     planner = Planner(scenario, device=local, seed=args.seed_base)
     ext = torch.cuda.ExternalStream(planner.stream(), device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -202,7 +205,7 @@ def run_b200(args, scenario):
 
     for i in range(args.warmup):
         planner.reset(args.seed_base + 100000 + i)
-        planner.solve(budget)
+        planner.solve(budget, iters)
 
     # ---- timed region (device) ----
     prof0 = planner.profile()
@@ -217,7 +220,7 @@ def run_b200(args, scenario):
             with torch.cuda.stream(ext):
                 flush.zero_()
             planner.reset(sd)
-            results.append(planner.solve(budget))
+            results.append(planner.solve(budget, iters))
         e1.record(ext)
         torch.cuda.synchronize()
     if ws > 1:
@@ -242,7 +245,7 @@ def run_b200(args, scenario):
     for sd in seeds:
         t0 = time.perf_counter()
         planner.reset(sd, x_init=x_init)          # H2D: start state (pinned staging), seed
-        r = planner.solve(budget)                  # D2H: result/control block
+        r = planner.solve(budget, iters)           # D2H: result/control block
         p = planner.path() if r["found"] else None  # D2H: root->leaf chain
         t_e2e += time.perf_counter() - t0
         e2e_props += r["propagations_attempted"]
@@ -253,7 +256,7 @@ def run_b200(args, scenario):
     for sd in seeds:
         t0 = time.perf_counter()
         planner.reset(sd, x_init=x_init)
-        r = planner.solve(budget)
+        r = planner.solve(max(budget, 1.0), 0)
         ttfs_wall.append((time.perf_counter() - t0) * 1e3 if r["found"] else float("nan"))
     planner.set_stop_at_first_solution(False)
     e = torch.tensor([t_e2e, float(e2e_props)], dtype=torch.float64, device=dev)
@@ -272,7 +275,7 @@ def run_b200(args, scenario):
         planner.set_profiling(True)
         pa = planner.profile()
         planner.reset(seeds[0])
-        planner.solve(budget)
+        planner.solve(budget, iters)
         pb = planner.profile()
         planner.set_profiling(False)
         roof = roofline(scenario, pa, pb)
@@ -395,6 +398,8 @@ def main():
     ap.add_argument("--config", default="forest_di6",
                     choices=["forest_di6", "narrow_dubins6", "building_quad12", "zigzag2d", "free2d"])
     ap.add_argument("--budget-ms", type=float, default=100.0)
+    ap.add_argument("--iters", type=int, default=0, help="fixed iterations per step instead of a time budget "
+                                                          "(profiling runs; not the headline workload)")
     ap.add_argument("--seed-base", type=int, default=1000)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -306,6 +307,108 @@ bool host_state_valid(const KpProblem& P, const std::vector<float>& boxes, const
     return true;
 }
 
+// Environment blob: obstacles as float4 + an exact broad-phase cell grid over
+// the workspace.  Cells per dim ~ workspace extent / median obstacle extent
+// (<= 32), shrunk until <= 8192 cells and <= 65535 list entries; every
+// obstacle is listed in every cell its AABB (expanded by a margin of 1e-3
+// cell, far above the fp32 error of the device's cell computation) touches.
+std::vector<uint8_t> build_env(KpProblem& P, const std::vector<float>& boxes, const std::vector<float>& spheres) {
+    const int nb = P.n_box, ns = P.n_sph, no = nb + ns;
+    std::vector<std::array<double, 6>> aabb(no);
+    for (int i = 0; i < nb; ++i)
+        for (int d = 0; d < 3; ++d) {
+            aabb[i][d] = boxes[6 * i + d];
+            aabb[i][3 + d] = boxes[6 * i + 3 + d];
+        }
+    for (int i = 0; i < ns; ++i) {
+        const double r = std::sqrt(static_cast<double>(spheres[4 * i + 3]));
+        for (int d = 0; d < 3; ++d) {
+            aabb[nb + i][d] = spheres[4 * i + d] - r;
+            aabb[nb + i][3 + d] = spheres[4 * i + d] + r;
+        }
+    }
+    int n[3] = {1, 1, 1};
+    double lo[3] = {0, 0, 0}, cell[3] = {1, 1, 1};
+    for (int d = 0; d < P.ws_dim; ++d) {
+        lo[d] = P.wlo[d];
+        const double ext = static_cast<double>(P.whi[d]) - lo[d];
+        std::vector<double> sz;
+        for (int i = 0; i < no; ++i) sz.push_back(std::min(ext, std::max(1e-9, aabb[i][3 + d] - aabb[i][d])));
+        double med = ext;
+        if (!sz.empty()) {
+            std::nth_element(sz.begin(), sz.begin() + sz.size() / 2, sz.end());
+            med = sz[sz.size() / 2];
+        }
+        n[d] = std::max(1, std::min(32, static_cast<int>(std::lround(ext / med))));
+        if (no == 0 || !(ext > 0)) n[d] = 1;
+    }
+    std::vector<std::vector<uint16_t>> lists;
+    for (;;) {
+        const int nc = n[0] * n[1] * n[2];
+        lists.assign(nc, {});
+        size_t entries = 0;
+        for (int d = 0; d < 3; ++d) cell[d] = d < P.ws_dim ? (static_cast<double>(P.whi[d]) - lo[d]) / n[d] : 1.0;
+        for (int i = 0; i < no; ++i) {
+            int r0[3], r1[3];
+            for (int d = 0; d < 3; ++d) {
+                if (d >= P.ws_dim) { r0[d] = 0; r1[d] = 0; continue; }
+                const double m = 1e-3 * cell[d];
+                const double a = std::isfinite(aabb[i][d]) ? (aabb[i][d] - m - lo[d]) / cell[d] : -1.0;
+                const double b = std::isfinite(aabb[i][3 + d]) ? (aabb[i][3 + d] + m - lo[d]) / cell[d] : n[d];
+                r0[d] = std::max(0, std::min(n[d] - 1, static_cast<int>(std::floor(a))));
+                r1[d] = std::max(0, std::min(n[d] - 1, static_cast<int>(std::floor(b))));
+            }
+            for (int z = r0[2]; z <= r1[2]; ++z)
+                for (int y = r0[1]; y <= r1[1]; ++y)
+                    for (int x = r0[0]; x <= r1[0]; ++x) {
+                        lists[x + n[0] * (y + n[1] * z)].push_back(static_cast<uint16_t>(i));
+                        ++entries;
+                    }
+        }
+        if ((nc <= 8192 && entries < 65535) || nc == 1) {
+            if (entries >= 65535) throw KpError(KP_ERR_SCHEMA, "too many obstacle cell entries");
+            break;
+        }
+        int dm = 0;
+        for (int d = 1; d < 3; ++d)
+            if (n[d] > n[dm]) dm = d;
+        n[dm] = std::max(1, n[dm] / 2);
+    }
+    const int nc = n[0] * n[1] * n[2];
+    for (int d = 0; d < 3; ++d) {
+        P.bg_n[d] = n[d];
+        P.bg_lo[d] = d < P.ws_dim ? static_cast<float>(lo[d]) : 0.0f;
+        P.bg_inv[d] = d < P.ws_dim ? static_cast<float>(1.0 / cell[d]) : 0.0f;
+    }
+    std::vector<uint16_t> start(nc + 1, 0), ids;
+    for (int c = 0; c < nc; ++c) {
+        start[c] = static_cast<uint16_t>(ids.size());
+        ids.insert(ids.end(), lists[c].begin(), lists[c].end());
+    }
+    start[nc] = static_cast<uint16_t>(ids.size());
+    P.n_cells = nc;
+    P.n_entries = static_cast<int32_t>(ids.size());
+    auto pad16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t obj_bytes = 16 * static_cast<size_t>(2 * nb + ns);
+    P.off_cstart = static_cast<uint32_t>(obj_bytes);
+    P.off_cids = static_cast<uint32_t>(pad16(obj_bytes + 2 * start.size()));
+    P.env_bytes = static_cast<uint32_t>(pad16(P.off_cids + 2 * std::max<size_t>(ids.size(), 1)));
+    if (P.env_bytes > 200 * 1024) throw KpError(KP_ERR_SCHEMA, "environment does not fit in shared memory");
+    std::vector<uint8_t> blob(P.env_bytes, 0);
+    float* f = reinterpret_cast<float*>(blob.data());
+    for (int i = 0; i < nb; ++i) {
+        for (int d = 0; d < 3; ++d) {
+            f[4 * i + d] = boxes[6 * i + d];
+            f[4 * (nb + i) + d] = boxes[6 * i + 3 + d];
+        }
+    }
+    for (int i = 0; i < ns; ++i)
+        for (int d = 0; d < 4; ++d) f[4 * (2 * nb + i) + d] = spheres[4 * i + d];
+    std::memcpy(blob.data() + P.off_cstart, start.data(), 2 * start.size());
+    if (!ids.empty()) std::memcpy(blob.data() + P.off_cids, ids.data(), 2 * ids.size());
+    return blob;
+}
+
 void capture_graph(kp_planner* pl) {
     cudaGraph_t g = nullptr;
     cuda_check(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
@@ -475,14 +578,10 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         B.max_tiles = static_cast<uint32_t>((max_e + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS);
         B.tile_sums = pl->dalloc<uint32_t>(3ull * B.max_tiles);
         B.tile_prefix = pl->dalloc<uint32_t>(3ull * B.max_tiles);
-        float* db = pl->dalloc<float>(boxes.size());
-        float* ds = pl->dalloc<float>(spheres.size());
-        if (!boxes.empty())
-            cuda_check(cudaMemcpy(db, boxes.data(), boxes.size() * 4, cudaMemcpyHostToDevice), "boxes H2D");
-        if (!spheres.empty())
-            cuda_check(cudaMemcpy(ds, spheres.data(), spheres.size() * 4, cudaMemcpyHostToDevice), "spheres H2D");
-        B.boxes = db;
-        B.spheres = ds;
+        const std::vector<uint8_t> blob = build_env(pl->P, boxes, spheres);
+        float4* denv = pl->dalloc<float4>(blob.size() / 16);
+        cuda_check(cudaMemcpy(denv, blob.data(), blob.size(), cudaMemcpyHostToDevice), "env H2D");
+        B.env = denv;
         B.ctl = pl->dalloc<KpCtl>(1);
         B.x0 = pl->dalloc<float>(KP_MAX_N);
         void* hx = nullptr;

@@ -43,25 +43,23 @@ KP_DEV unsigned long long globaltimer() {
     return t;
 }
 
-// Stage obstacles into shared memory (boxes then spheres).
-KP_DEV void stage_obstacles(const KpProblem& P, const KpBuffers& B, float* sbox, float* ssph) {
-    for (int i = threadIdx.x; i < P.n_box * 6; i += blockDim.x) sbox[i] = B.boxes[i];
-    for (int i = threadIdx.x; i < P.n_sph * 4; i += blockDim.x) ssph[i] = B.spheres[i];
+// Stage the environment blob into shared memory (16-byte vector copies).
+KP_DEV Env stage_env(const KpProblem& P, const KpBuffers& B, float4* smem) {
+    for (uint32_t i = threadIdx.x; i < P.env_bytes / 16; i += blockDim.x) smem[i] = B.env[i];
     __syncthreads();
+    return env_view(P, smem);
 }
 
 template <int MODEL>
 __global__ void __launch_bounds__(256) k_propagate(KpProblem P, KpBuffers B) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
-    extern __shared__ float smem[];
-    float* sbox = smem;
-    float* ssph = smem + 6 * P.n_box;
+    extern __shared__ float4 smem4[];
     __shared__ unsigned long long s_cnt[6];
     KpCtl* ctl = B.ctl;
     if (ctl->done) return;
     if (threadIdx.x < 6) s_cnt[threadIdx.x] = 0;
-    stage_obstacles(P, B, sbox, ssph);
+    const Env E = stage_env(P, B, smem4);
     const uint32_t n_items = ctl->n_items;
     const uint32_t it = ctl->iter;
     const unsigned long long seed = ctl->seed;
@@ -81,7 +79,7 @@ __global__ void __launch_bounds__(256) k_propagate(KpProblem P, KpBuffers B) {
             for (int d = 0; d < N; ++d) x[d] = B.state[static_cast<size_t>(d) * cap + node];
             const float acc_p = __uint_as_float(B.acc[node]);
             ItemOut o;
-            const int rc = propagate_item<MODEL>(P, sbox, ssph, x, acc_p, seed, it, node, br, u, dt, o);
+            const int rc = propagate_item<MODEL>(P, E, x, acc_p, seed, it, node, br, u, dt, o);
             c[2] += o.steps;
             c[3] += o.interp;
             c[4] += o.nbox;
@@ -222,6 +220,8 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
     const uint32_t n_items = ctl->n_items;
     const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
     const uint32_t n_tiles = (E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
+    const uint32_t n_part = min(gridDim.x, n_tiles);  // participating blocks
+    if (blockIdx.x >= n_part) return;
     const uint32_t* __restrict__ live = B.live[it & 1];
     uint32_t term = 0, deact = 0, react = 0, hops = 0, nlive = 0, nslot = 0, nadm = 0;
     if (threadIdx.x < 7) s_st[threadIdx.x] = 0;
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
         if (s_st[5]) atomicAdd(&ctl->stats.slots_scanned, static_cast<unsigned long long>(s_st[5]));
         if (s_st[6]) atomicAdd(&ctl->stats.admitted_checked, static_cast<unsigned long long>(s_st[6]));
         __threadfence();
-        s_last = (atomicAdd(&ctl->ticket_a, 1u) == gridDim.x - 1);
+        s_last = (atomicAdd(&ctl->ticket_a, 1u) == n_part - 1);
     }
     __syncthreads();
     if (!s_last) return;
@@ -321,6 +321,8 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     const uint32_t n_items = ctl->n_items;
     const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
     const uint32_t n_tiles = ctl->n_tiles;
+    const uint32_t n_part = min(gridDim.x, n_tiles);
+    if (blockIdx.x >= n_part) return;
     const uint32_t tot_keep = ctl->tot_keep, tot_va = ctl->tot_va, accepted = ctl->accepted;
     const uint32_t n_nodes = ctl->n_nodes;
     const uint32_t cap = P.capacity, S = P.max_slots;
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(&ctl->ticket_b, 1u) == gridDim.x - 1);
+    if (threadIdx.x == 0) s_last = (atomicAdd(&ctl->ticket_b, 1u) == n_part - 1);
     __syncthreads();
     if (!s_last || threadIdx.x != 0) return;
     __threadfence();
@@ -433,7 +435,6 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
         __threadfence_system();
         *B.host_done = 1;
     }
-    __threadfence_system();
 }
 
 // Reset the region table and plant the root (Alg. 1 lines 1-5).
@@ -495,14 +496,14 @@ __global__ void k_debug_propagate(KpProblem P, KpBuffers B, uint32_t n, const fl
                                   uint8_t* goals) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
-    extern __shared__ float smem[];
-    stage_obstacles(P, B, smem, smem + 6 * P.n_box);
+    extern __shared__ float4 smem4[];
+    const Env E = stage_env(P, B, smem4);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float x[N], u[M], dt;
     for (int d = 0; d < N; ++d) x[d] = ps[static_cast<size_t>(i) * N + d];
     ItemOut o;
-    const int rc = propagate_item<MODEL>(P, smem, smem + 6 * P.n_box, x, pacc[i], B.ctl->seed, it, ids[i], brs[i], u, dt, o);
+    const int rc = propagate_item<MODEL>(P, E, x, pacc[i], B.ctl->seed, it, ids[i], brs[i], u, dt, o);
     valid[i] = rc == 0 ? 1 : (rc == 1 ? 0 : 2);
     for (int d = 0; d < N; ++d) xs[static_cast<size_t>(i) * N + d] = rc == 0 ? x[d] : 0.0f;
     for (int d = 0; d < M; ++d) us[static_cast<size_t>(i) * M + d] = u[d];
@@ -582,7 +583,7 @@ __global__ void k_reintegrate(KpProblem P, KpBuffers B, const int32_t* chain, ui
 // ------------------------------------------------------------------------
 namespace kp {
 
-size_t propagate_smem(const KpProblem& P) { return sizeof(float) * (6 * P.n_box + 4 * P.n_sph); }
+size_t propagate_smem(const KpProblem& P) { return P.env_bytes; }
 
 cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_prop, int grid_sel, cudaStream_t st,
                              int which) {

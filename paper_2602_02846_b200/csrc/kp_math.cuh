@@ -208,32 +208,56 @@ KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk) {
 }
 
 // --------------------------------------------------------- environment ----
-// Position inside some closed obstacle?  Obstacles staged in shared memory;
-// every lane reads the same primitive at the same time (broadcast).  `tests`
-// accumulates the primitive tests executed (roofline accounting; boxes in
-// the low 32 bits' role via two counters).
-KP_DEV bool in_obstacle(const float* __restrict__ sbox, int n_box, const float* __restrict__ ssph, int n_sph,
-                        float px, float py, float pz, uint32_t& nbox, uint32_t& nsph) {
-    for (int b = 0; b < n_box; ++b) {
-        const float* o = sbox + 6 * b;
-        if (px >= o[0] && px <= o[3] && py >= o[1] && py <= o[4] && pz >= o[2] && pz <= o[5]) {
-            nbox += b + 1;
-            return true;
+// Environment view over the shared-memory copy of the blob (kp_types.h).
+struct Env {
+    const float4* blo;
+    const float4* bhi;
+    const float4* sph;
+    const uint16_t* cstart;
+    const uint16_t* cids;
+};
+
+KP_DEV Env env_view(const KpProblem& P, const float4* base) {
+    Env e;
+    e.blo = base;
+    e.bhi = base + P.n_box;
+    e.sph = base + 2 * P.n_box;
+    e.cstart = reinterpret_cast<const uint16_t*>(reinterpret_cast<const char*>(base) + P.off_cstart);
+    e.cids = reinterpret_cast<const uint16_t*>(reinterpret_cast<const char*>(base) + P.off_cids);
+    return e;
+}
+
+KP_DEV int bg_cell(const KpProblem& P, float v, int d) {
+    int c = __float2int_rd((v - P.bg_lo[d]) * P.bg_inv[d]);
+    c = c < 0 ? 0 : c;
+    return c >= P.bg_n[d] ? P.bg_n[d] - 1 : c;
+}
+
+// Position inside some closed obstacle?  Broad phase: the
+// point's cell list; narrow phase: the exact closed box / sphere test, boxes
+// read as two float4 (no short-circuit chains of dependent loads).  nbox /
+// nsph accumulate the narrow-phase tests executed (roofline accounting).
+KP_DEV bool in_obstacle(const KpProblem& P, const Env& E, float px, float py, float pz, uint32_t& nbox,
+                        uint32_t& nsph) {
+    const int c = bg_cell(P, px, 0) + P.bg_n[0] * (bg_cell(P, py, 1) + P.bg_n[1] * bg_cell(P, pz, 2));
+    const int b = E.cstart[c], e = E.cstart[c + 1];
+    for (int k = b; k < e; ++k) {
+        const int id = E.cids[k];
+        if (id < P.n_box) {
+            const float4 lo = E.blo[id], hi = E.bhi[id];
+            ++nbox;
+            const bool in = (px >= lo.x) & (px <= hi.x) & (py >= lo.y) & (py <= hi.y) & (pz >= lo.z) & (pz <= hi.z);
+            if (in) return true;
+        } else {
+            const float4 o = E.sph[id - P.n_box];
+            ++nsph;
+            const float dx = px - o.x, dy = py - o.y, dz = pz - o.z;
+            float d2 = dx * dx;
+            d2 = fmaf(dy, dy, d2);
+            d2 = fmaf(dz, dz, d2);
+            if (d2 <= o.w) return true;
         }
     }
-    nbox += n_box;
-    for (int s = 0; s < n_sph; ++s) {
-        const float* o = ssph + 4 * s;
-        const float dx = px - o[0], dy = py - o[1], dz = pz - o[2];
-        float d2 = dx * dx;
-        d2 = fmaf(dy, dy, d2);
-        d2 = fmaf(dz, dz, d2);
-        if (d2 <= o[3]) {
-            nsph += s + 1;
-            return true;
-        }
-    }
-    nsph += n_sph;
     return false;
 }
 
@@ -309,8 +333,7 @@ struct ItemOut {
 // the candidate state on a valid exit.  Returns 0 valid, 1 invalid, 2 diverged.
 // The parent (samples[0]) is not re-checked: it is a stored valid node.
 template <int MODEL>
-KP_DEV int propagate_item(const KpProblem& P, const float* __restrict__ sbox, const float* __restrict__ ssph,
-                          float* x, float acc_parent, uint64_t seed, uint32_t it, uint32_t node, uint32_t br,
+KP_DEV int propagate_item(const KpProblem& P, const Env& E, float* x, float acc_parent, uint64_t seed, uint32_t it, uint32_t node, uint32_t br,
                           float* u, float& dt, ItemOut& o) {
     constexpr int M = Model<MODEL>::M;
     constexpr bool TWO_D = (MODEL == 0);
@@ -331,7 +354,7 @@ KP_DEV int propagate_item(const KpProblem& P, const float* __restrict__ sbox, co
         o.steps += 1;
         const float nx = x[0], ny = x[1], nz = TWO_D ? 0.0f : x[2];
         if (!within_bounds<MODEL>(P, x)) return 1;
-        if (in_obstacle(sbox, P.n_box, ssph, P.n_sph, nx, ny, nz, o.nbox, o.nsph)) return 1;
+        if (in_obstacle(P, E, nx, ny, nz, o.nbox, o.nsph)) return 1;
         const float dx = nx - px, dy = ny - py, dz = nz - pz;
         float d2 = dx * dx;
         d2 = fmaf(dy, dy, d2);
@@ -343,8 +366,8 @@ KP_DEV int propagate_item(const KpProblem& P, const float* __restrict__ sbox, co
             for (int j = 1; j < k; ++j) {
                 const float t = static_cast<float>(j) / static_cast<float>(k);
                 o.interp += 1;
-                if (in_obstacle(sbox, P.n_box, ssph, P.n_sph, fmaf(t, dx, px), fmaf(t, dy, py),
-                                TWO_D ? 0.0f : fmaf(t, dz, pz), o.nbox, o.nsph))
+                if (in_obstacle(P, E, fmaf(t, dx, px), fmaf(t, dy, py), TWO_D ? 0.0f : fmaf(t, dz, pz), o.nbox,
+                                o.nsph))
                     return 1;
             }
         }

@@ -52,6 +52,17 @@ struct KpProblem {
     uint32_t capacity;       // t_e
     uint32_t max_slots;      // V_U slot buffer (multiple of 32)
     float x_init[KP_MAX_N];
+    // environment blob (staged into shared memory by k_propagate):
+    //   float4 box_lo[n_box], float4 box_hi[n_box], float4 sph[n_sph] (c xyz, r^2),
+    //   uint16 cell_start[n_cells + 1] (padded to 16 B), uint16 cell_ids[n_entries]
+    // cell grid = exact broad phase: every obstacle whose (margin-expanded)
+    // AABB overlaps a cell is listed in it, so the narrow-phase verdict equals
+    // testing every obstacle ("outside every obstacle").
+    float bg_lo[3], bg_inv[3];
+    int32_t bg_n[3];
+    int32_t n_cells, n_entries;
+    uint32_t env_bytes;        // multiple of 16
+    uint32_t off_cstart, off_cids;  // byte offsets inside the blob
 };
 
 struct KpStats {
@@ -121,9 +132,7 @@ struct KpBuffers {
     uint32_t* tile_sums;    // [3][max_tiles]
     uint32_t* tile_prefix;  // [3][max_tiles]
     uint32_t max_tiles;
-    // obstacles: boxes [n_box][6] (lo xyz, hi xyz), spheres [n_sph][4] (c xyz, r^2)
-    const float* boxes;
-    const float* spheres;
+    const float4* env;      // environment blob (see KpProblem)
     float* x0;              // [KP_MAX_N] current query's start state (H2D per query)
     KpCtl* ctl;
     volatile uint32_t* host_done;  // mapped pinned word (device writes 1 at termination)
