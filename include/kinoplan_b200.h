@@ -266,6 +266,18 @@ typedef struct kp_profile {
 int kp_set_profiling(kp_planner* planner, int enabled);
 int kp_get_profile(kp_planner* planner, kp_profile* out);
 
+/* Per-iteration trace (tracing aux subsystem): one record per iteration
+ * boundary since the last reset, newest KP_TRACE_CAP kept.  t_ns is device
+ * time since solve start (%globaltimer); items = lambda*|V_A| propagated in
+ * that iteration; live / frontier / nodes are the counts after it. */
+#define KP_TRACE_CAP 8192
+typedef struct kp_trace_entry {
+    uint64_t t_ns;
+    uint32_t iteration, items, live, frontier, nodes, committed;
+} kp_trace_entry;
+
+int kp_get_trace(kp_planner* planner, kp_trace_entry* buf, size_t cap, size_t* len);
+
 /* The CUDA stream (cudaStream_t) every kernel of this handle is launched on,
  * so a caller can bracket work with its own CUDA events. */
 int kp_get_stream(kp_planner* planner, void** stream);

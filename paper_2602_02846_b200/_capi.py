@@ -135,6 +135,11 @@ class Profile(C.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class TraceEntry(C.Structure):
+    _fields_ = [("t_ns", C.c_uint64), ("iteration", C.c_uint32), ("items", C.c_uint32), ("live", C.c_uint32),
+                ("frontier", C.c_uint32), ("nodes", C.c_uint32), ("committed", C.c_uint32)]
+
+
 class TimelineEntry(C.Structure):
     _fields_ = [("iteration", C.c_uint64), ("elapsed_s", C.c_double), ("cost", C.c_double), ("leaf", C.c_int64)]
 
@@ -305,6 +310,8 @@ def load_library() -> C.CDLL:
     L.kp_set_profiling.restype = I
     L.kp_get_profile.argtypes = [P, CP(Profile)]
     L.kp_get_profile.restype = I
+    L.kp_get_trace.argtypes = [P, CP(TraceEntry), C.c_size_t, CP(C.c_size_t)]
+    L.kp_get_trace.restype = I
     L.kp_get_stream.argtypes = [P, CP(C.c_void_p)]
     L.kp_get_stream.restype = I
     L.kp_abi_version.argtypes = []
@@ -317,7 +324,7 @@ EXPORTED_SYMBOLS = [
     "kp_create", "kp_destroy", "kp_last_error", "kp_reset", "kp_reset_query", "kp_set_stop_at_first_solution",
     "kp_solve", "kp_get_timeline", "kp_get_path",
     "kp_get_trajectory", "kp_get_nodes", "kp_get_region_table", "kp_get_grid", "kp_debug_propagate",
-    "kp_set_profiling", "kp_get_profile", "kp_get_stream", "kp_solve_batch", "kp_abi_version",
+    "kp_set_profiling", "kp_get_profile", "kp_get_trace", "kp_get_stream", "kp_solve_batch", "kp_abi_version",
 ]
 
 

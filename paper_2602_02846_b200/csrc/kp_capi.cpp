@@ -584,6 +584,7 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         B.env = denv;
         B.ctl = pl->dalloc<KpCtl>(1);
         B.x0 = pl->dalloc<float>(KP_MAX_N);
+        B.trace = pl->dalloc<KpTraceRec>(KP_TRACE_CAP);
         void* hx = nullptr;
         cuda_check(cudaHostAlloc(&hx, sizeof(float) * KP_MAX_N, cudaHostAllocDefault), "cudaHostAlloc x0");
         pl->h_x0 = static_cast<float*>(hx);
@@ -668,6 +669,25 @@ int kp_get_profile(kp_planner* pl, kp_profile* out) {
         out->ancestor_hops = st.ancestor_hops;
         out->slots_scanned = st.slots_scanned;
         out->admitted_checked = st.admitted_checked;
+    });
+}
+
+int kp_get_trace(kp_planner* pl, kp_trace_entry* buf, size_t cap, size_t* len) {
+    if (!pl || !len) return KP_ERR_ARGUMENT;
+    return guard(pl, [&] {
+        fetch_ctl(pl);
+        const uint32_t n = std::min<uint32_t>(pl->ctl.iter, KP_TRACE_CAP);
+        *len = n;
+        if (!buf || cap == 0) return;
+        std::vector<KpTraceRec> all(KP_TRACE_CAP);
+        cuda_check(cudaMemcpyAsync(all.data(), pl->B.trace, sizeof(KpTraceRec) * KP_TRACE_CAP, cudaMemcpyDeviceToHost,
+                                   pl->stream), "trace D2H");
+        cuda_check(cudaStreamSynchronize(pl->stream), "trace sync");
+        const uint32_t first = pl->ctl.iter - n;  // oldest kept iteration index
+        for (uint32_t k = 0; k < std::min<size_t>(cap, n); ++k) {
+            const KpTraceRec& r = all[(first + k) % KP_TRACE_CAP];
+            buf[k] = {r.t_ns, r.iteration, r.items, r.live, r.frontier, r.nodes, r.committed};
+        }
     });
 }
 

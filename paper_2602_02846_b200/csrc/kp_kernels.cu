@@ -417,6 +417,16 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
         ctl->best_ns = now - ctl->t_start_ns;
         ctl->best_iter = it1;
     }
+    {
+        KpTraceRec& tr = B.trace[it % KP_TRACE_CAP];
+        tr.t_ns = now - ctl->t_start_ns;
+        tr.iteration = it1;
+        tr.items = n_items;
+        tr.live = ctl->n_live;
+        tr.frontier = ctl->n_va;
+        tr.nodes = ctl->n_nodes;
+        tr.committed = accepted;
+    }
     bool done = false;
     if (items > S) {
         ctl->error = 8;  // KP_ERR_SLOT_OVERFLOW

@@ -79,6 +79,12 @@ struct KpTimeline {
     unsigned long long best;  // (cost bits << 32) | leaf
 };
 
+#define KP_TRACE_CAP 8192
+struct KpTraceRec {
+    unsigned long long t_ns;
+    uint32_t iteration, items, live, frontier, nodes, committed;
+};
+
 struct KpCtl {
     // current iteration's lists (parity = iter & 1)
     uint32_t iter;            // iterations completed since reset
@@ -133,6 +139,7 @@ struct KpBuffers {
     uint32_t* tile_prefix;  // [3][max_tiles]
     uint32_t max_tiles;
     const float4* env;      // environment blob (see KpProblem)
+    KpTraceRec* trace;      // [KP_TRACE_CAP] ring, one record per iteration boundary
     float* x0;              // [KP_MAX_N] current query's start state (H2D per query)
     KpCtl* ctl;
     volatile uint32_t* host_done;  // mapped pinned word (device writes 1 at termination)

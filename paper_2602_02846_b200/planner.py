@@ -201,6 +201,16 @@ class Planner:
         self._check(self._lib.kp_get_profile(self._h, C.byref(pr)))
         return pr.as_dict()
 
+    def trace(self) -> np.ndarray:
+        """Per-iteration device trace: structured array (t_ns, iteration, items, live, frontier, nodes, committed)."""
+        n = C.c_size_t()
+        self._check(self._lib.kp_get_trace(self._h, None, 0, C.byref(n)))
+        buf = (_capi.TraceEntry * max(1, n.value))()
+        self._check(self._lib.kp_get_trace(self._h, buf, n.value, C.byref(n)))
+        dt = np.dtype([("t_ns", np.uint64), ("iteration", np.uint32), ("items", np.uint32), ("live", np.uint32),
+                       ("frontier", np.uint32), ("nodes", np.uint32), ("committed", np.uint32)])
+        return np.frombuffer(bytes(buf)[: n.value * dt.itemsize], dtype=dt).copy()
+
     def stream(self) -> int:
         s = C.c_void_p()
         self._check(self._lib.kp_get_stream(self._h, C.byref(s)))
