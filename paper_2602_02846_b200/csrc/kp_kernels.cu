@@ -50,64 +50,145 @@ KP_DEV Env stage_env(const KpProblem& P, const KpBuffers& B, float4* smem) {
     return env_view(P, smem);
 }
 
+// Propagate (Alg. 2).  Work is claimed by blocks in chunks of 256*G slots
+// (dynamic cursor).  Per chunk: (1) every thread draws (u, dt) for G slots
+// (convergent RNG) into shared memory; (2) block counting sort of the chunk
+// by RK4 step count S, longest first; (3) each warp integrates groups of 32
+// consecutive sorted slots, so lanes of a warp run nearly the same number of
+// steps (SIMT efficiency) — the result of a slot does not depend on which
+// lane runs it.  Admitted slots write their record and set their admit/goal
+// bit with atomicOr (the consumers zero the words after use).
+#define KP_PROP_THREADS 256
+#define KP_PROP_MAXG 4
+#define KP_SORT_BUCKETS 64
+
 template <int MODEL>
-__global__ void __launch_bounds__(256) k_propagate(KpProblem P, KpBuffers B) {
+struct PropSmem {
+    float u[Model<MODEL>::M][KP_PROP_THREADS * KP_PROP_MAXG];
+    float dt[KP_PROP_THREADS * KP_PROP_MAXG];
+    uint32_t node[KP_PROP_THREADS * KP_PROP_MAXG];
+    uint16_t steps[KP_PROP_THREADS * KP_PROP_MAXG];
+    uint16_t perm[KP_PROP_THREADS * KP_PROP_MAXG];
+    uint32_t hist[KP_SORT_BUCKETS];
+    uint32_t chunk;
+    unsigned long long cnt[6];
+};
+
+template <int MODEL>
+__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propagate(KpProblem P, KpBuffers B) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
     extern __shared__ float4 smem4[];
-    __shared__ unsigned long long s_cnt[6];
+    __shared__ PropSmem<MODEL> sh;
     KpCtl* ctl = B.ctl;
     if (ctl->done) return;
-    if (threadIdx.x < 6) s_cnt[threadIdx.x] = 0;
-    const Env E = stage_env(P, B, smem4);
     const uint32_t n_items = ctl->n_items;
+    const uint32_t G = min(KP_PROP_MAXG, max(1u, n_items / (KP_PROP_THREADS * gridDim.x)));
+    const uint32_t CH = KP_PROP_THREADS * G;
+    const uint32_t n_chunks = (n_items + CH - 1) / CH;
+    if (blockIdx.x >= n_chunks) return;  // nothing for this block this iteration
+    if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
+    const Env E = stage_env(P, B, smem4);
     const uint32_t it = ctl->iter;
     const unsigned long long seed = ctl->seed;
     const uint32_t* __restrict__ va = B.va[it & 1];
-    const uint32_t padded = (n_items + 31u) & ~31u;
-    const uint32_t cap = P.capacity, S = P.max_slots;
+    const uint32_t cap = P.capacity, S_cap = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};  // valid, admitted, steps, interp, box tests, sphere tests
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < padded; i += gridDim.x * blockDim.x) {
-        bool adm = false, goal = false;
-        if (i < n_items) {
-            const uint32_t f = i / lam;
-            const uint32_t br = i - f * lam;
-            const uint32_t node = va[f];
-            float x[N], u[M], dt;
+    if (threadIdx.x == 0) sh.chunk = blockIdx.x;  // first chunk is static, the rest dynamic
+    __syncthreads();
+    for (;;) {
+        const uint32_t chunk = sh.chunk;
+        if (chunk >= n_chunks) break;
+        const uint32_t c0 = chunk * CH;
+        if (threadIdx.x < KP_SORT_BUCKETS) sh.hist[threadIdx.x] = 0;
+        __syncthreads();
+        // (1) draw (u, dt) and the step count of every slot of the chunk
+        for (uint32_t k = 0; k < G; ++k) {
+            const uint32_t p = k * KP_PROP_THREADS + threadIdx.x;
+            const uint32_t i = c0 + p;
+            uint32_t key = 0;
+            if (i < n_items) {
+                const uint32_t f = i / lam;
+                const uint32_t br = i - f * lam;
+                const uint32_t node = va[f];
+                float u[M], dt;
+                sample_item<M>(P, seed, it, node, br, u, dt);
+                const int S = step_count(P, dt);
+#pragma unroll
+                for (int d = 0; d < M; ++d) sh.u[d][p] = u[d];
+                sh.dt[p] = dt;
+                sh.node[p] = node;
+                sh.steps[p] = static_cast<uint16_t>(min(S, 65535));
+                key = static_cast<uint32_t>(min(S, KP_SORT_BUCKETS - 1));
+            }
+            sh.perm[p] = static_cast<uint16_t>(key);  // temporarily the bucket key
+            atomicAdd(&sh.hist[KP_SORT_BUCKETS - 1 - key], 1u);
+        }
+        __syncthreads();
+        // (2) exclusive scan of the 64 buckets (descending S), then scatter
+        if (warp == 0) {
+            uint32_t a = sh.hist[2 * lane], b = sh.hist[2 * lane + 1];
+            uint32_t x = a + b;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+                if (lane >= off) x += y;
+            }
+            const uint32_t excl = x - a - b;
+            sh.hist[2 * lane] = excl;
+            sh.hist[2 * lane + 1] = excl + a;
+        }
+        __syncthreads();
+        uint32_t keys[KP_PROP_MAXG];
+        for (uint32_t k = 0; k < G; ++k) keys[k] = sh.perm[k * KP_PROP_THREADS + threadIdx.x];
+        __syncthreads();
+        for (uint32_t k = 0; k < G; ++k) {
+            const uint32_t p = k * KP_PROP_THREADS + threadIdx.x;
+            const uint32_t pos = atomicAdd(&sh.hist[KP_SORT_BUCKETS - 1 - keys[k]], 1u);
+            sh.perm[pos] = static_cast<uint16_t>(p);
+        }
+        __syncthreads();
+        // (3) integrate groups of 32 consecutive sorted slots per warp
+        for (uint32_t k = 0; k < G; ++k) {
+            const uint32_t pos = (k * (KP_PROP_THREADS / 32) + warp) * 32 + lane;
+            const uint32_t p = sh.perm[pos];
+            const uint32_t i = c0 + p;
+            if (i >= n_items) continue;
+            const uint32_t node = sh.node[p];
+            float x[N], u[M];
 #pragma unroll
             for (int d = 0; d < N; ++d) x[d] = B.state[static_cast<size_t>(d) * cap + node];
+#pragma unroll
+            for (int d = 0; d < M; ++d) u[d] = sh.u[d][p];
+            const float dt = sh.dt[p];
             const float acc_p = __uint_as_float(B.acc[node]);
             ItemOut o;
-            const int rc = propagate_item<MODEL>(P, E, x, acc_p, seed, it, node, br, u, dt, o);
+            const int rc = integrate_item<MODEL>(P, E, x, u, dt, sh.steps[p], acc_p, o);
             c[2] += o.steps;
             c[3] += o.interp;
             c[4] += o.nbox;
             c[5] += o.nsph;
-            if (rc == 0) {
-                ++c[0];
-                const uint32_t bits = __float_as_uint(o.acc);
-                const uint32_t old = atomicMin(B.rc + o.region, bits);
-                adm = bits <= old;  // Improved or Equal
-                if (adm) {
-                    ++c[1];
-                    goal = o.goal;
+            if (rc != 0) continue;
+            ++c[0];
+            const uint32_t bits = __float_as_uint(o.acc);
+            const uint32_t old = atomicMin(B.rc + o.region, bits);
+            if (bits > old) continue;  // Worse: discarded (Improved / Equal admitted)
+            ++c[1];
 #pragma unroll
-                    for (int d = 0; d < N; ++d) B.vu_state[static_cast<size_t>(d) * S + i] = x[d];
+            for (int d = 0; d < N; ++d) B.vu_state[static_cast<size_t>(d) * S_cap + i] = x[d];
 #pragma unroll
-                    for (int d = 0; d < M; ++d) B.vu_ctrl[static_cast<size_t>(d) * S + i] = u[d];
-                    B.vu_dt[i] = dt;
-                    B.vu_acc[i] = bits;
-                    B.vu_region[i] = o.region;
-                }
-            }
+            for (int d = 0; d < M; ++d) B.vu_ctrl[static_cast<size_t>(d) * S_cap + i] = u[d];
+            B.vu_dt[i] = dt;
+            B.vu_acc[i] = bits;
+            B.vu_region[i] = o.region;
+            atomicOr(B.admit_mask + (i >> 5), 1u << (i & 31));
+            if (o.goal) atomicOr(B.goal_mask + (i >> 5), 1u << (i & 31));
         }
-        const uint32_t am = __ballot_sync(0xFFFFFFFFu, adm);
-        const uint32_t gm = __ballot_sync(0xFFFFFFFFu, goal);
-        if ((threadIdx.x & 31) == 0) {
-            B.admit_mask[i >> 5] = am;
-            B.goal_mask[i >> 5] = gm;
-        }
+        __syncthreads();
+        if (threadIdx.x == 0) sh.chunk = gridDim.x + atomicAdd(&ctl->prop_cursor, 1u);
+        __syncthreads();
     }
     // warp-aggregated then block-aggregated counters
 #pragma unroll
@@ -115,19 +196,19 @@ __global__ void __launch_bounds__(256) k_propagate(KpProblem P, KpBuffers B) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) c[k] += __shfl_down_sync(0xFFFFFFFFu, c[k], off);
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < 6; ++k)
-            if (c[k]) atomicAdd(&s_cnt[k], static_cast<unsigned long long>(c[k]));
+            if (c[k]) atomicAdd(&sh.cnt[k], static_cast<unsigned long long>(c[k]));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (s_cnt[0]) atomicAdd(&ctl->stats.valid, s_cnt[0]);
-        if (s_cnt[1]) atomicAdd(&ctl->stats.admitted, s_cnt[1]);
-        if (s_cnt[2]) atomicAdd(&ctl->stats.rk4_steps, s_cnt[2]);
-        if (s_cnt[3]) atomicAdd(&ctl->stats.interp_points, s_cnt[3]);
-        if (s_cnt[4]) atomicAdd(&ctl->stats.box_tests, s_cnt[4]);
-        if (s_cnt[5]) atomicAdd(&ctl->stats.sphere_tests, s_cnt[5]);
+        if (sh.cnt[0]) atomicAdd(&ctl->stats.valid, sh.cnt[0]);
+        if (sh.cnt[1]) atomicAdd(&ctl->stats.admitted, sh.cnt[1]);
+        if (sh.cnt[2]) atomicAdd(&ctl->stats.rk4_steps, sh.cnt[2]);
+        if (sh.cnt[3]) atomicAdd(&ctl->stats.interp_points, sh.cnt[3]);
+        if (sh.cnt[4]) atomicAdd(&ctl->stats.box_tests, sh.cnt[4]);
+        if (sh.cnt[5]) atomicAdd(&ctl->stats.sphere_tests, sh.cnt[5]);
     }
 }
 
@@ -246,7 +327,10 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
         }
         // slot elements are warp-aligned (live part padded to 32)
         const uint32_t cm = __ballot_sync(0xFFFFFFFFu, commit);
-        if (e >= live_pad && e < E && (threadIdx.x & 31) == 0) B.commit_mask[(e - live_pad) >> 5] = cm;
+        if (e >= live_pad && e < E && (threadIdx.x & 31) == 0) {
+            B.commit_mask[(e - live_pad) >> 5] = cm;
+            B.admit_mask[(e - live_pad) >> 5] = 0u;  // consumed: ready for the next propagate
+        }
         Cnt3 tot;
         block_scan3(x, &tot);
         if (threadIdx.x == 0) {
@@ -349,8 +433,10 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
                 x.c = (B.commit_mask[s >> 5] >> (s & 31)) & 1u;
             }
         }
+        const bool goal = is_slot && x.c && ((B.goal_mask[s >> 5] >> (s & 31)) & 1u);
         Cnt3 tot;
-        const Cnt3 inc = block_scan3(x, &tot);
+        const Cnt3 inc = block_scan3(x, &tot);  // (barrier: every lane has read its goal bit)
+        if (e >= live_pad && e < E && (threadIdx.x & 31) == 0) B.goal_mask[(e - live_pad) >> 5] = 0u;
         const uint32_t pk = B.tile_prefix[tile] + inc.k - x.k;
         const uint32_t pv = B.tile_prefix[B.max_tiles + tile] + inc.v - x.v;
         const uint32_t pc = B.tile_prefix[2 * B.max_tiles + tile] + inc.c - x.c;
@@ -375,7 +461,7 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
             B.icnt[id] = 0;
             live_n[tot_keep + pc] = id;
             va_n[tot_va + pc] = id;
-            if ((B.goal_mask[s >> 5] >> (s & 31)) & 1u)  // Alg. 4 lines 5-7
+            if (goal)  // Alg. 4 lines 5-7
                 atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
         }
     }
@@ -440,6 +526,7 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     if (ctl->stop_first && best != ~0ull) done = true;
     if (ctl->n_live == 0) done = true;
     ctl->ticket_b = 0;
+    ctl->prop_cursor = 0;
     if (done) {
         ctl->done = 1;
         __threadfence_system();
@@ -491,6 +578,7 @@ __global__ void k_start(KpBuffers B, unsigned long long budget_ns, uint32_t max_
     ctl->stop_first = stop_first;
     ctl->ticket_a = 0;
     ctl->ticket_b = 0;
+    ctl->prop_cursor = 0;
     bool done = ctl->error != 0 || ctl->n_live == 0 || (stop_first && ctl->best != ~0ull);
     ctl->done = done ? 1u : 0u;
     __threadfence_system();
@@ -600,10 +688,10 @@ cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_pr
     const size_t smem = propagate_smem(P);
     if (which & 1) {
         switch (P.model) {
-            case 0: k_propagate<0><<<grid_prop, 256, smem, st>>>(P, B); break;
-            case 1: k_propagate<1><<<grid_prop, 256, smem, st>>>(P, B); break;
-            case 2: k_propagate<2><<<grid_prop, 256, smem, st>>>(P, B); break;
-            default: k_propagate<3><<<grid_prop, 256, smem, st>>>(P, B); break;
+                case 0: k_propagate<0><<<grid_prop, KP_PROP_THREADS, smem, st>>>(P, B); break;
+            case 1: k_propagate<1><<<grid_prop, KP_PROP_THREADS, smem, st>>>(P, B); break;
+            case 2: k_propagate<2><<<grid_prop, KP_PROP_THREADS, smem, st>>>(P, B); break;
+            default: k_propagate<3><<<grid_prop, KP_PROP_THREADS, smem, st>>>(P, B); break;
         }
     }
     if (which & 2) k_select_reduce<<<grid_sel, KP_SELECT_THREADS, 0, st>>>(P, B);
@@ -613,7 +701,6 @@ cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_pr
 
 cudaError_t set_propagate_smem(const KpProblem& P) {
     const int smem = static_cast<int>(propagate_smem(P));
-    if (smem <= 48 * 1024) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     switch (P.model) {
         case 0: e = cudaFuncSetAttribute(k_propagate<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
@@ -628,16 +715,18 @@ int propagate_occupancy(const KpProblem& P) {
     int nb = 0;
     const size_t smem = propagate_smem(P);
     switch (P.model) {
-        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<0>, 256, smem); break;
-        case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<1>, 256, smem); break;
-        case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<2>, 256, smem); break;
-        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<3>, 256, smem); break;
+        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<0>, KP_PROP_THREADS, smem); break;
+        case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<1>, KP_PROP_THREADS, smem); break;
+        case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<2>, KP_PROP_THREADS, smem); break;
+        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<3>, KP_PROP_THREADS, smem); break;
     }
     return nb;
 }
 
 cudaError_t launch_reset(const KpProblem& P, const KpBuffers& B, unsigned long long seed, cudaStream_t st) {
     cudaMemsetAsync(B.ctl, 0, sizeof(KpCtl), st);
+    cudaMemsetAsync(B.admit_mask, 0, sizeof(uint32_t) * (P.max_slots / 32), st);
+    cudaMemsetAsync(B.goal_mask, 0, sizeof(uint32_t) * (P.max_slots / 32), st);
     k_reset_table<<<148 * 4, 256, 0, st>>>(P, B);
     k_reset_root<<<1, 32, 0, st>>>(P, B, seed);
     return cudaGetLastError();

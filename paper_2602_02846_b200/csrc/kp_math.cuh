@@ -176,9 +176,11 @@ KP_DEV void derivative(const KpProblem& P, const float* x, const float* u, float
 }
 
 // One classical RK4 step with constant control, then angle wrap.
-// Returns false when a coordinate is non-finite (propagation diverged).
+// `sixth` must equal hk / 6.0f (IEEE division; hoisted by the caller for the
+// full-length steps).  Returns false when a coordinate is non-finite
+// (propagation diverged).
 template <int MODEL>
-KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk) {
+KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk, float sixth) {
     constexpr int N = Model<MODEL>::N;
     float k1[N], k2[N], k3[N], k4[N], t[N];
     const float half = 0.5f * hk;
@@ -192,7 +194,6 @@ KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk) {
 #pragma unroll
     for (int i = 0; i < N; ++i) t[i] = fmaf(hk, k3[i], x[i]);
     derivative<MODEL>(P, t, u, k4);
-    const float sixth = hk / 6.0f;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         const float a = k1[i] + k4[i];
@@ -205,6 +206,17 @@ KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk) {
 #pragma unroll
     for (int i = 0; i < N; ++i) ok = ok && isfinite(x[i]);
     return ok;
+}
+
+template <int MODEL>
+KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk) {
+    return rk4_step<MODEL>(P, x, u, hk, hk / 6.0f);
+}
+
+// Number of RK4 steps of a segment: samples at 0, h, ..., dt.
+KP_DEV int step_count(const KpProblem& P, float dt) {
+    const int S = static_cast<int>(ceilf(dt / P.h));
+    return S < 1 ? 1 : S;
 }
 
 // --------------------------------------------------------- environment ----
@@ -326,31 +338,29 @@ struct ItemOut {
     bool goal;
 };
 
-// One work item of Alg. 2 lines 3-7: sample (u, dt), RK4
-// rollout streamed in registers, every sample validated and every
-// interpolated point (spacing <= collision_step) obstacle-checked, path length
-// accumulated, region of the end state.  x holds the parent state on entry and
-// the candidate state on a valid exit.  Returns 0 valid, 1 invalid, 2 diverged.
-// The parent (samples[0]) is not re-checked: it is a stored valid node.
+// Rollout + validity + cost of one work item whose (u, dt) are drawn (Alg. 2
+// lines 4-7): RK4 rollout streamed in registers, every
+// sample validated and every interpolated point (spacing <= collision_step)
+// obstacle-checked, path length accumulated, region of the end state.  x holds
+// the parent state on entry and the candidate state on a valid exit.  Returns
+// 0 valid, 1 invalid, 2 diverged.  The parent (samples[0]) is not re-checked:
+// it is a stored valid node.
 template <int MODEL>
-KP_DEV int propagate_item(const KpProblem& P, const Env& E, float* x, float acc_parent, uint64_t seed, uint32_t it, uint32_t node, uint32_t br,
-                          float* u, float& dt, ItemOut& o) {
-    constexpr int M = Model<MODEL>::M;
+KP_DEV int integrate_item(const KpProblem& P, const Env& E, float* x, const float* u, float dt, int S, float acc_parent,
+                          ItemOut& o) {
     constexpr bool TWO_D = (MODEL == 0);
-    sample_item<M>(P, seed, it, node, br, u, dt);
-    const float q = dt / P.h;
-    int S = static_cast<int>(ceilf(q));
-    if (S < 1) S = 1;
     float px = x[0], py = x[1], pz = TWO_D ? 0.0f : x[2];
     float total = 0.0f;
     o.steps = 0;
     o.interp = 0;
     o.nbox = 0;
     o.nsph = 0;
+    const float h6 = P.h / 6.0f;
     for (int s = 0; s < S; ++s) {
-        const float hk = (s + 1 < S) ? P.h : dt - static_cast<float>(S - 1) * P.h;
+        const bool last = s + 1 >= S;
+        const float hk = last ? dt - static_cast<float>(S - 1) * P.h : P.h;
         if (!(hk > 0.0f)) break;
-        if (!rk4_step<MODEL>(P, x, u, hk)) return 2;
+        if (!rk4_step<MODEL>(P, x, u, hk, last ? hk / 6.0f : h6)) return 2;
         o.steps += 1;
         const float nx = x[0], ny = x[1], nz = TWO_D ? 0.0f : x[2];
         if (!within_bounds<MODEL>(P, x)) return 1;
@@ -381,6 +391,14 @@ KP_DEV int propagate_item(const KpProblem& P, const Env& E, float* x, float acc_
     o.region = region_index<Model<MODEL>::N>(P, x);
     o.goal = in_goal<Model<MODEL>::N>(P, x);
     return 0;
+}
+
+// One whole work item of Alg. 2 lines 3-7: sample (u, dt), then integrate.
+template <int MODEL>
+KP_DEV int propagate_item(const KpProblem& P, const Env& E, float* x, float acc_parent, uint64_t seed, uint32_t it,
+                          uint32_t node, uint32_t br, float* u, float& dt, ItemOut& o) {
+    sample_item<Model<MODEL>::M>(P, seed, it, node, br, u, dt);
+    return integrate_item<MODEL>(P, E, x, u, dt, step_count(P, dt), acc_parent, o);
 }
 
 }  // namespace kp
