@@ -274,6 +274,10 @@ int kp_get_profile(kp_planner* planner, kp_profile* out);
 typedef struct kp_trace_entry {
     uint64_t t_ns;
     uint32_t iteration, items, live, frontier, nodes, committed;
+    /* in-graph kernel stamps, ns since solve start: block-0 entry of
+     * propagate / select_reduce / select_scatter, last-block exit of
+     * select_reduce (t_ns is the scatter's last block = the boundary) */
+    uint32_t t_prop, t_sel, t_sel_end, t_scat;
 } kp_trace_entry;
 
 int kp_get_trace(kp_planner* planner, kp_trace_entry* buf, size_t cap, size_t* len);

@@ -137,7 +137,8 @@ class Profile(C.Structure):
 
 class TraceEntry(C.Structure):
     _fields_ = [("t_ns", C.c_uint64), ("iteration", C.c_uint32), ("items", C.c_uint32), ("live", C.c_uint32),
-                ("frontier", C.c_uint32), ("nodes", C.c_uint32), ("committed", C.c_uint32)]
+                ("frontier", C.c_uint32), ("nodes", C.c_uint32), ("committed", C.c_uint32),
+                ("t_prop", C.c_uint32), ("t_sel", C.c_uint32), ("t_sel_end", C.c_uint32), ("t_scat", C.c_uint32)]
 
 
 class TimelineEntry(C.Structure):

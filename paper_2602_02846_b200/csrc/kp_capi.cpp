@@ -686,7 +686,8 @@ int kp_get_trace(kp_planner* pl, kp_trace_entry* buf, size_t cap, size_t* len) {
         const uint32_t first = pl->ctl.iter - n;  // oldest kept iteration index
         for (uint32_t k = 0; k < std::min<size_t>(cap, n); ++k) {
             const KpTraceRec& r = all[(first + k) % KP_TRACE_CAP];
-            buf[k] = {r.t_ns, r.iteration, r.items, r.live, r.frontier, r.nodes, r.committed};
+            buf[k] = {r.t_ns, r.iteration, r.items, r.live, r.frontier, r.nodes, r.committed,
+                      r.t_prop, r.t_sel, r.t_sel_end, r.t_scat};
         }
     });
 }

@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propa
     __shared__ PropSmem<MODEL> sh;
     KpCtl* ctl = B.ctl;
     if (ctl->done) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
     const uint32_t n_items = ctl->n_items;
     const uint32_t G = min(KP_PROP_MAXG, max(1u, n_items / (KP_PROP_THREADS * gridDim.x)));
     const uint32_t CH = KP_PROP_THREADS * G;
@@ -293,6 +294,7 @@ KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, ui
 __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P, KpBuffers B) {
     KpCtl* ctl = B.ctl;
     if (ctl->done) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_sel_ns = globaltimer();
     __shared__ unsigned int s_last;
     __shared__ uint32_t s_st[7];
     const uint32_t it = ctl->iter;
@@ -391,6 +393,7 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
         ctl->tot_commit = carry.c;
         ctl->accepted = carry.c < remaining ? carry.c : remaining;
         ctl->ticket_a = 0;
+        ctl->t_sel_end_ns = globaltimer();
         __threadfence();
     }
 }
@@ -398,6 +401,7 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
 __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem P, KpBuffers B) {
     KpCtl* ctl = B.ctl;
     if (ctl->done) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_scat_ns = globaltimer();
     __shared__ unsigned int s_last;
     const uint32_t it = ctl->iter;
     const uint32_t n_live = ctl->n_live;
@@ -512,6 +516,11 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
         tr.frontier = ctl->n_va;
         tr.nodes = ctl->n_nodes;
         tr.committed = accepted;
+        const unsigned long long t0 = ctl->t_start_ns;
+        tr.t_prop = static_cast<uint32_t>(ctl->t_prop_ns - t0);
+        tr.t_sel = static_cast<uint32_t>(ctl->t_sel_ns - t0);
+        tr.t_sel_end = static_cast<uint32_t>(ctl->t_sel_end_ns - t0);
+        tr.t_scat = static_cast<uint32_t>(ctl->t_scat_ns - t0);
     }
     bool done = false;
     if (items > S) {

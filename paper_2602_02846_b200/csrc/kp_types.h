@@ -83,6 +83,10 @@ struct KpTimeline {
 struct KpTraceRec {
     unsigned long long t_ns;
     uint32_t iteration, items, live, frontier, nodes, committed;
+    // in-graph kernel timestamps (ns since solve start): block 0 entry of
+    // propagate / select_reduce / select_scatter and the last-block exit of
+    // select_reduce; the boundary itself is t_ns (scatter last block)
+    uint32_t t_prop, t_sel, t_sel_end, t_scat;
 };
 
 struct KpCtl {
@@ -106,6 +110,7 @@ struct KpCtl {
     unsigned long long best;  // (cost bits << 32) | leaf ; init ~0
     unsigned long long t_start_ns, deadline_ns, t_last_ns;
     unsigned long long first_ns, best_ns;
+    unsigned long long t_prop_ns, t_sel_ns, t_sel_end_ns, t_scat_ns;  // current iteration stamps
     KpStats stats;
     KpTimeline timeline[KP_TIMELINE_CAP];
 };

@@ -208,7 +208,8 @@ class Planner:
         buf = (_capi.TraceEntry * max(1, n.value))()
         self._check(self._lib.kp_get_trace(self._h, buf, n.value, C.byref(n)))
         dt = np.dtype([("t_ns", np.uint64), ("iteration", np.uint32), ("items", np.uint32), ("live", np.uint32),
-                       ("frontier", np.uint32), ("nodes", np.uint32), ("committed", np.uint32)])
+                       ("frontier", np.uint32), ("nodes", np.uint32), ("committed", np.uint32),
+                       ("t_prop", np.uint32), ("t_sel", np.uint32), ("t_sel_end", np.uint32), ("t_scat", np.uint32)])
         return np.frombuffer(bytes(buf)[: n.value * dt.itemsize], dtype=dt).copy()
 
     def stream(self) -> int:

@@ -1,4 +1,5 @@
-"""Per-iteration device trace of one query (graph mode, no profiler)."""
+"""Per-iteration device trace of one query (graph mode, no profiler): time per
+iteration split into propagate / select_reduce / select_scatter / gaps."""
 import sys
 import numpy as np
 sys.path.insert(0, '.')
@@ -13,12 +14,19 @@ with Planner(s, seed=1000) as g:
     g.reset(1000)
     r = g.solve(budget)
     tr = g.trace()
-    t = tr['t_ns'].astype(np.float64) / 1e3
-    d = np.diff(np.concatenate([[0.0], t]))
-    print(scene, 'iterations', r['iterations'], 'first sol it', r['first_solution_iteration'], 'ttfs_ms', r['first_solution_s'] * 1e3)
-    print('it  dt_us  items  live  frontier  nodes  committed')
-    for k in list(range(0, min(40, len(tr)))) + list(range(40, len(tr), max(1, len(tr) // 30))):
+    t_end = tr['t_ns'].astype(np.float64) / 1e3
+    t_prev = np.concatenate([[0.0], t_end[:-1]])
+    tp, ts, tse, tsc = (tr[k].astype(np.float64) / 1e3 for k in ('t_prop', 't_sel', 't_sel_end', 't_scat'))
+    prop, sel, gap2, scat, gap1 = ts - tp, tse - ts, tsc - tse, t_end - tsc, tp - t_prev
+    print(scene, 'iterations', r['iterations'], 'first sol it', r['first_solution_iteration'],
+          'ttfs_ms %.3f' % (r['first_solution_s'] * 1e3))
+    print('  it  total   gap  prop   sel  gap  scat    items   live frontier')
+    rows = list(range(0, min(30, len(tr)))) + list(range(30, len(tr), max(1, len(tr) // 20)))
+    for k in rows:
         e = tr[k]
-        print(f"{e['iteration']:5d} {d[k]:7.1f} {e['items']:8d} {e['live']:7d} {e['frontier']:7d} {e['nodes']:8d} {e['committed']:6d}")
-    big = tr['items'] > 100000
-    print('mean dt_us small(<2k items): %.1f' % d[tr['items'] < 2000].mean(), ' large(>100k): %.1f' % (d[big].mean() if big.any() else -1))
+        print(f"{e['iteration']:4d} {t_end[k]-t_prev[k]:6.1f} {gap1[k]:5.1f} {prop[k]:5.1f} {sel[k]:5.1f} {gap2[k]:4.1f} "
+              f"{scat[k]:5.1f} {e['items']:8d} {e['live']:6d} {e['frontier']:6d}")
+    for name, m in (('small(<2k items)', tr['items'] < 2000), ('large(>100k)', tr['items'] > 100000)):
+        if m.any():
+            print(f"mean {name}: total {np.mean((t_end-t_prev)[m]):.1f}  gap {gap1[m].mean():.1f}  prop {prop[m].mean():.1f}  "
+                  f"sel {sel[m].mean():.1f}  gap2 {gap2[m].mean():.1f}  scat {scat[m].mean():.1f}")
