@@ -349,7 +349,6 @@ template <int MODEL>
 KP_DEV int integrate_item(const KpProblem& P, const Env& E, float* x, const float* u, float dt, int S, float acc_parent,
                           ItemOut& o) {
     constexpr bool TWO_D = (MODEL == 0);
-    constexpr int W = 4;  // register window: W RK4 steps, then W independent point checks
     float px = x[0], py = x[1], pz = TWO_D ? 0.0f : x[2];
     float total = 0.0f;
     o.steps = 0;
@@ -357,64 +356,33 @@ KP_DEV int integrate_item(const KpProblem& P, const Env& E, float* x, const floa
     o.nbox = 0;
     o.nsph = 0;
     const float h6 = P.h / 6.0f;
-    int s = 0;
-    while (s < S) {
-        float wx[W], wy[W], wz[W];
-        int nw = 0;
-        // (a) integrate up to W steps: a pure FP chain (state bounds are register compares)
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            if (s < S) {
-                const bool last = s + 1 >= S;
-                const float hk = last ? dt - static_cast<float>(S - 1) * P.h : P.h;
-                if (!(hk > 0.0f)) {
-                    S = s;  // degenerate last step: the segment ends at the previous sample
-                } else {
-                    if (!rk4_step<MODEL>(P, x, u, hk, last ? hk / 6.0f : h6)) return 2;
-                    o.steps += 1;
-                    if (!within_bounds<MODEL>(P, x)) return 1;
-                    wx[k] = x[0];
-                    wy[k] = x[1];
-                    wz[k] = TWO_D ? 0.0f : x[2];
-                    nw = k + 1;
-                    ++s;
-                }
+    for (int s = 0; s < S; ++s) {
+        const bool last = s + 1 >= S;
+        const float hk = last ? dt - static_cast<float>(S - 1) * P.h : P.h;
+        if (!(hk > 0.0f)) break;
+        if (!rk4_step<MODEL>(P, x, u, hk, last ? hk / 6.0f : h6)) return 2;
+        o.steps += 1;
+        const float nx = x[0], ny = x[1], nz = TWO_D ? 0.0f : x[2];
+        if (!within_bounds<MODEL>(P, x)) return 1;
+        if (in_obstacle(P, E, nx, ny, nz, o.nbox, o.nsph)) return 1;
+        const float dx = nx - px, dy = ny - py, dz = nz - pz;
+        float d2 = dx * dx;
+        d2 = fmaf(dy, dy, d2);
+        if (!TWO_D) d2 = fmaf(dz, dz, d2);
+        const float d = sqrtf(d2);
+        if (d > P.coll) {  // dyadic subdivision (nested points)
+            int k = 2;
+            while (d / static_cast<float>(k) > P.coll && k < (1 << 24)) k <<= 1;
+            for (int j = 1; j < k; ++j) {
+                const float t = static_cast<float>(j) / static_cast<float>(k);
+                o.interp += 1;
+                if (in_obstacle(P, E, fmaf(t, dx, px), fmaf(t, dy, py), TWO_D ? 0.0f : fmaf(t, dz, pz), o.nbox,
+                                o.nsph))
+                    return 1;
             }
         }
-        // (b) the window's samples: obstacle test + dyadic interpolation, independent chains
-        bool hit = false;
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            if (k < nw) {
-                const float ax = k == 0 ? px : wx[k - 1], ay = k == 0 ? py : wy[k - 1], az = k == 0 ? pz : wz[k - 1];
-                hit = hit || in_obstacle(P, E, wx[k], wy[k], wz[k], o.nbox, o.nsph);
-                const float dx = wx[k] - ax, dy = wy[k] - ay, dz = wz[k] - az;
-                float d2 = dx * dx;
-                d2 = fmaf(dy, dy, d2);
-                if (!TWO_D) d2 = fmaf(dz, dz, d2);
-                const float d = sqrtf(d2);
-                if (!hit && d > P.coll) {  // dyadic subdivision (nested points)
-                    int kk = 2;
-                    while (d / static_cast<float>(kk) > P.coll && kk < (1 << 24)) kk <<= 1;
-                    for (int j = 1; j < kk && !hit; ++j) {
-                        const float t = static_cast<float>(j) / static_cast<float>(kk);
-                        o.interp += 1;
-                        hit = in_obstacle(P, E, fmaf(t, dx, ax), fmaf(t, dy, ay), TWO_D ? 0.0f : fmaf(t, dz, az),
-                                          o.nbox, o.nsph);
-                    }
-                }
-                total += d;  // cost.hpp:59-61, summed in sample order
-            }
-        }
-        if (hit) return 1;
-#pragma unroll
-        for (int k = 0; k < W; ++k) {  // last sample of the window (static indices: stays in registers)
-            if (k + 1 == nw) {
-                px = wx[k];
-                py = wy[k];
-                pz = wz[k];
-            }
-        }
+        total += d;  // cost.hpp:59-61 (position head == workspace dims for every built-in model)
+        px = nx; py = ny; pz = nz;
     }
     float seg;
     if (P.cost_kind == 1) seg = dt;                        // control_duration
