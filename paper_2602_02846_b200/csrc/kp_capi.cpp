@@ -173,6 +173,16 @@ void build_problem(const kp_problem_desc* p, const kp_config_desc* c, KpProblem&
             P.whi[i] = std::numeric_limits<float>::infinity();
         }
     }
+    P.check_finite = 0;
+    for (int i = 0; i < n; ++i) {
+        P.blo[i] = P.slo[i];
+        P.bhi[i] = P.shi[i];
+        if (i < ws) {
+            P.blo[i] = std::max(P.blo[i], P.wlo[i]);
+            P.bhi[i] = std::min(P.bhi[i], P.whi[i]);
+        }
+        if (!std::isfinite(P.blo[i]) || !std::isfinite(P.bhi[i])) P.check_finite = 1;
+    }
     if (p->n_obstacles < 0 || p->n_obstacles > KP_MAX_OBSTACLES)
         throw KpError(KP_ERR_SCHEMA, "obstacle count out of range");
     for (int i = 0; i < p->n_obstacles; ++i) {
@@ -380,18 +390,19 @@ std::vector<uint8_t> build_env(KpProblem& P, const std::vector<float>& boxes, co
         P.bg_lo[d] = d < P.ws_dim ? static_cast<float>(lo[d]) : 0.0f;
         P.bg_inv[d] = d < P.ws_dim ? static_cast<float>(1.0 / cell[d]) : 0.0f;
     }
-    std::vector<uint16_t> start(nc + 1, 0), ids;
+    std::vector<uint32_t> range(nc, 0);
+    std::vector<uint16_t> ids;
     for (int c = 0; c < nc; ++c) {
-        start[c] = static_cast<uint16_t>(ids.size());
+        const uint32_t b = static_cast<uint32_t>(ids.size());
         ids.insert(ids.end(), lists[c].begin(), lists[c].end());
+        range[c] = b | (static_cast<uint32_t>(ids.size()) << 16);
     }
-    start[nc] = static_cast<uint16_t>(ids.size());
     P.n_cells = nc;
     P.n_entries = static_cast<int32_t>(ids.size());
     auto pad16 = [](size_t x) { return (x + 15) & ~size_t(15); };
     const size_t obj_bytes = 16 * static_cast<size_t>(2 * nb + ns);
-    P.off_cstart = static_cast<uint32_t>(obj_bytes);
-    P.off_cids = static_cast<uint32_t>(pad16(obj_bytes + 2 * start.size()));
+    P.off_cells = static_cast<uint32_t>(obj_bytes);
+    P.off_cids = static_cast<uint32_t>(pad16(obj_bytes + 4 * range.size()));
     P.env_bytes = static_cast<uint32_t>(pad16(P.off_cids + 2 * std::max<size_t>(ids.size(), 1)));
     if (P.env_bytes > 200 * 1024) throw KpError(KP_ERR_SCHEMA, "environment does not fit in shared memory");
     std::vector<uint8_t> blob(P.env_bytes, 0);
@@ -404,7 +415,7 @@ std::vector<uint8_t> build_env(KpProblem& P, const std::vector<float>& boxes, co
     }
     for (int i = 0; i < ns; ++i)
         for (int d = 0; d < 4; ++d) f[4 * (2 * nb + i) + d] = spheres[4 * i + d];
-    std::memcpy(blob.data() + P.off_cstart, start.data(), 2 * start.size());
+    std::memcpy(blob.data() + P.off_cells, range.data(), 4 * range.size());
     if (!ids.empty()) std::memcpy(blob.data() + P.off_cids, ids.data(), 2 * ids.size());
     return blob;
 }
@@ -561,6 +572,7 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         B.region = pl->dalloc<uint32_t>(cap);
         B.status = pl->dalloc<uint8_t>(cap);
         B.icnt = pl->dalloc<uint16_t>(cap);
+        B.link = pl->dalloc<uint4>(cap);
         B.rc = pl->dalloc<uint32_t>(n_regions);
         for (int i = 0; i < 2; ++i) {
             B.live[i] = pl->dalloc<uint32_t>(cap);

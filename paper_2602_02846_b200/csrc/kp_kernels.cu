@@ -75,7 +75,7 @@ struct PropSmem {
 };
 
 template <int MODEL>
-__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propagate(KpProblem P, KpBuffers B) {
+__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 5)) k_propagate(KpProblem P, KpBuffers B) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
     extern __shared__ float4 smem4[];
@@ -274,13 +274,23 @@ KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, ui
         B.icnt[g] = static_cast<uint16_t>(ic);
         return KP_ST_INACTIVE;
     }
-    // (3) Active: some ancestor no longer region-minimal -> Inactive
+    // (3) Active: some ancestor no longer region-minimal -> Inactive.  The walk
+    // is software-pipelined over 16-byte node links: the next hop's link load
+    // is issued together with this hop's region-cost load, so the chain costs
+    // about one L2 round trip per hop.
     bool dominated = P.deact != 0;
     int32_t p = B.parent[g];
-    while (!dominated && p >= 0) {
-        ++*hops;
-        if (B.acc[p] > B.rc[B.region[p]]) dominated = true;
-        p = B.parent[p];
+    if (!dominated && p >= 0) {
+        uint4 L = B.link[p];  // {parent, region, acc, -}
+        for (;;) {
+            ++*hops;
+            const int32_t q = static_cast<int32_t>(L.x);
+            uint4 Ln = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+            if (q >= 0) Ln = B.link[q];
+            if (L.z > B.rc[L.y]) { dominated = true; break; }
+            if (q < 0) break;
+            L = Ln;
+        }
     }
     if (dominated) {
         B.status[g] = KP_ST_INACTIVE;
@@ -459,8 +469,11 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
             const uint32_t abits = B.vu_acc[s];
             B.dt[id] = B.vu_dt[s];
             B.acc[id] = abits;
-            B.region[id] = B.vu_region[s];
-            B.parent[id] = static_cast<int32_t>(va[s / lam]);
+            const uint32_t par = va[s / lam];
+            const uint32_t reg = B.vu_region[s];
+            B.region[id] = reg;
+            B.parent[id] = static_cast<int32_t>(par);
+            B.link[id] = make_uint4(par, reg, abits, 0u);
             B.status[id] = KP_ST_ACTIVE;
             B.icnt[id] = 0;
             live_n[tot_keep + pc] = id;
@@ -564,6 +577,7 @@ __global__ void k_reset_root(KpProblem P, KpBuffers B, unsigned long long seed) 
     B.acc[0] = 0u;
     B.parent[0] = -1;
     B.region[0] = r;
+    B.link[0] = make_uint4(0xFFFFFFFFu, r, 0u, 0u);
     B.status[0] = KP_ST_ACTIVE;
     B.icnt[0] = 0;
     B.rc[r] = 0u;  // DECISION: root region seeded with cost 0 (SPEC.md:425 region dominance)

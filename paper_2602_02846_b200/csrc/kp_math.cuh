@@ -202,6 +202,7 @@ KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk, flo
     }
 #pragma unroll
     for (int i = 0; i < Model<MODEL>::NA; ++i) x[Model<MODEL>::A0 + i] = wrap_angle(x[Model<MODEL>::A0 + i]);
+    if (!P.check_finite) return true;  // finite bounds reject inf / NaN in within_bounds anyway
     bool ok = true;
 #pragma unroll
     for (int i = 0; i < N; ++i) ok = ok && isfinite(x[i]);
@@ -225,7 +226,7 @@ struct Env {
     const float4* blo;
     const float4* bhi;
     const float4* sph;
-    const uint16_t* cstart;
+    const uint32_t* cells;
     const uint16_t* cids;
 };
 
@@ -234,12 +235,13 @@ KP_DEV Env env_view(const KpProblem& P, const float4* base) {
     e.blo = base;
     e.bhi = base + P.n_box;
     e.sph = base + 2 * P.n_box;
-    e.cstart = reinterpret_cast<const uint16_t*>(reinterpret_cast<const char*>(base) + P.off_cstart);
+    e.cells = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(base) + P.off_cells);
     e.cids = reinterpret_cast<const uint16_t*>(reinterpret_cast<const char*>(base) + P.off_cids);
     return e;
 }
 
 KP_DEV int bg_cell(const KpProblem& P, float v, int d) {
+    if (P.bg_n[d] == 1) return 0;  // uniform branch: undivided dimension
     int c = __float2int_rd((v - P.bg_lo[d]) * P.bg_inv[d]);
     c = c < 0 ? 0 : c;
     return c >= P.bg_n[d] ? P.bg_n[d] - 1 : c;
@@ -252,7 +254,8 @@ KP_DEV int bg_cell(const KpProblem& P, float v, int d) {
 KP_DEV bool in_obstacle(const KpProblem& P, const Env& E, float px, float py, float pz, uint32_t& nbox,
                         uint32_t& nsph) {
     const int c = bg_cell(P, px, 0) + P.bg_n[0] * (bg_cell(P, py, 1) + P.bg_n[1] * bg_cell(P, pz, 2));
-    const int b = E.cstart[c], e = E.cstart[c + 1];
+    const uint32_t range = E.cells[c];
+    const int b = static_cast<int>(range & 0xFFFFu), e = static_cast<int>(range >> 16);
     for (int k = b; k < e; ++k) {
         const int id = E.cids[k];
         if (id < P.n_box) {
@@ -278,12 +281,11 @@ KP_DEV bool in_obstacle(const KpProblem& P, const Env& E, float px, float py, fl
 template <int MODEL>
 KP_DEV bool within_bounds(const KpProblem& P, const float* x) {
     constexpr int N = Model<MODEL>::N;
+    // state bounds with the workspace bounds folded into the
+    // position dims on the host: x >= max(lo_s, lo_w) <=> x >= lo_s && x >= lo_w
     bool ok = true;
 #pragma unroll
-    for (int i = 0; i < N; ++i) ok = ok && (x[i] >= P.slo[i]) && (x[i] <= P.shi[i]);
-    constexpr int W = (MODEL == 0) ? 2 : 3;
-#pragma unroll
-    for (int i = 0; i < W; ++i) ok = ok && (x[i] >= P.wlo[i]) && (x[i] <= P.whi[i]);
+    for (int i = 0; i < N; ++i) ok = ok & (x[i] >= P.blo[i]) & (x[i] <= P.bhi[i]);
     return ok;
 }
 

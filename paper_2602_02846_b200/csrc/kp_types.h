@@ -36,6 +36,8 @@ struct KpProblem {
     int32_t cost_kind;       // 0 path length, 1 control duration
     int32_t cost_pos_dims;
     float slo[KP_MAX_N], shi[KP_MAX_N];
+    float blo[KP_MAX_N], bhi[KP_MAX_N];  // state bounds with the workspace folded into the position dims
+    int32_t check_finite;                // some folded bound is infinite: keep the explicit finite test
     float clo[KP_MAX_M], cw[KP_MAX_M];
     double clo_d[KP_MAX_M], chi_d[KP_MAX_M];
     float wlo[3], whi[3];
@@ -54,7 +56,7 @@ struct KpProblem {
     float x_init[KP_MAX_N];
     // environment blob (staged into shared memory by k_propagate):
     //   float4 box_lo[n_box], float4 box_hi[n_box], float4 sph[n_sph] (c xyz, r^2),
-    //   uint16 cell_start[n_cells + 1] (padded to 16 B), uint16 cell_ids[n_entries]
+    //   uint32 cell_range[n_cells] (start | end << 16), uint16 cell_ids[n_entries]
     // cell grid = exact broad phase: every obstacle whose (margin-expanded)
     // AABB overlaps a cell is listed in it, so the narrow-phase verdict equals
     // testing every obstacle ("outside every obstacle").
@@ -62,7 +64,7 @@ struct KpProblem {
     int32_t bg_n[3];
     int32_t n_cells, n_entries;
     uint32_t env_bytes;        // multiple of 16
-    uint32_t off_cstart, off_cids;  // byte offsets inside the blob
+    uint32_t off_cells, off_cids;  // byte offsets inside the blob
 };
 
 struct KpStats {
@@ -128,6 +130,7 @@ struct KpBuffers {
     uint16_t* icnt;
     // region table [n_regions], encoded fp32 bits (+inf = 0x7F800000)
     uint32_t* rc;
+    uint4* link;         // [capacity] {parent, region, acc bits, 0}: one 16-byte load per ancestor hop
     // lists, double-buffered [2][capacity]
     uint32_t* live[2];
     uint32_t* va[2];
