@@ -75,7 +75,7 @@ struct PropSmem {
 };
 
 template <int MODEL>
-__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 5)) k_propagate(KpProblem P, KpBuffers B) {
+__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propagate(KpProblem P, KpBuffers B) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
     extern __shared__ float4 smem4[];
