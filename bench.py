@@ -182,7 +182,7 @@ def run_reference(args, scenario):
 def run_b200(args, scenario):
     import torch
 
-    from paper_2602_02846_b200 import Planner
+    from paper_2602_02846_b200 import Planner, replicas
 
     ws, rank, local = _dist()
     if ws > 1:
@@ -201,7 +201,7 @@ def run_b200(args, scenario):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     n = planner.n
     x_init = scenario["problem"]["x_init"]
-    seeds = [args.seed_base + rank * args.steps + i for i in range(args.steps)]
+    seeds = replicas.shard_seeds(args.seed_base, rank, ws, args.steps)
 
     clk = ClockSampler(local).__enter__()  # sampler up before the timed region (NVML init is slow)
     for i in range(args.warmup):
@@ -236,15 +236,8 @@ def run_b200(args, scenario):
     prof1 = planner.profile()
     dev_ms = e0.elapsed_time(e1)
     props = sum(r["propagations_attempted"] for r in results)
-    t = torch.tensor([dev_ms, float(props)], dtype=torch.float64, device=dev)
-    if ws > 1:
-        mx = t.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        sm = t.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        dev_ms, props_total = float(mx[0]), float(sm[1])
-    else:
-        props_total = float(props)
+    dev_ms, props_total = replicas.reduce_job(dev_ms, props, world=ws, device=dev)
+    results = replicas.gather_results(results, world=ws)
     value = props_total / (dev_ms / 1e3)
 
     # ---- end-to-end through the public C-ABI with host buffers ----
@@ -267,15 +260,7 @@ def run_b200(args, scenario):
         r = planner.solve(max(budget, 1.0), 0)
         ttfs_wall.append((time.perf_counter() - t0) * 1e3 if r["found"] else float("nan"))
     planner.set_stop_at_first_solution(False)
-    e = torch.tensor([t_e2e, float(e2e_props)], dtype=torch.float64, device=dev)
-    if ws > 1:
-        emx = e.clone()
-        torch.distributed.all_reduce(emx, op=torch.distributed.ReduceOp.MAX)
-        esm = e.clone()
-        torch.distributed.all_reduce(esm, op=torch.distributed.ReduceOp.SUM)
-        t_e2e, e2e_total = float(emx[0]), float(esm[1])
-    else:
-        e2e_total = float(e2e_props)
+    t_e2e, e2e_total = replicas.reduce_job(t_e2e, e2e_props, world=ws, device=dev)
 
     # ---- per-kernel roofline pass (one query, per-launch CUDA events) ----
     roof = None
