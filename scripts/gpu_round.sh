@@ -1,21 +1,34 @@
 #!/bin/bash
-# One GPU session: tests, smoke, peaks, bench, ncu launch list + full capture.
-# Usage (under gpurun): bash scripts/gpu_round.sh [tag]
+# One GPU session: peaks, tests, smoke, bench (+reference arm), ncu launch list + full captures.
+# Usage (under gpurun): bash scripts/gpu_round.sh TAG
 set -u
 TAG=${1:-r1}
-OUT=gpurun_out
+OUT=gpurun_out/$TAG
 mkdir -p $OUT
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu_$TAG.txt 2>&1
-./tools/fp32_peak > $OUT/fp32_peak_$TAG.json 2> $OUT/fp32_peak_$TAG.err
-timeout 900 python -m pytest tests -m gpu -q > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu_$TAG.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke_$TAG.log
-timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?" >> $OUT/bench_$TAG.err
-#timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
-PCMD="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --iters 60"
-timeout 300 $PCMD > $OUT/plain_$TAG.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/launches_$TAG.csv $PCMD > $OUT/ncu_launch_$TAG.log 2>&1
-timeout 300 $PCMD > $OUT/plain2_$TAG.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_propagate -s 40 -c 2 -o $OUT/prof_prop_$TAG -f $PCMD > $OUT/ncu_full_$TAG.log 2>&1
-timeout 300 $PCMD > $OUT/plain3_$TAG.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_select -s 40 -c 4 -o $OUT/prof_sel_$TAG -f $PCMD > $OUT/ncu_sel_$TAG.log 2>&1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
+./tools/fp32_peak > $OUT/fp32_peak.json 2> $OUT/fp32_peak.err
+timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
+for cfg in narrow_dubins6 building_quad12; do
+  timeout 600 python bench.py --config $cfg --no-cpu-baseline > $OUT/bench_$cfg.json 2> $OUT/bench_$cfg.err
+done
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+python scripts/trace_gpu.py forest_di6 > $OUT/trace_forest_di6.txt 2>&1
+python scripts/trace_gpu.py building_quad12 1.0 > $OUT/trace_building_quad12.txt 2>&1
+python scripts/trace_gpu.py narrow_dubins6 > $OUT/trace_narrow_dubins6.txt 2>&1
+# launch list of a fixed-iteration query (the same command first without ncu)
+PCMD="python scripts/prof_run.py forest_di6 60"
+timeout 300 $PCMD > $OUT/plain_launch.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_forest_di6.csv $PCMD > $OUT/ncu_launch.log 2>&1
+# full captures of the steady-state kernels
+for spec in "forest_di6 40" "building_quad12 30" "narrow_dubins6 40"; do
+  set -- $spec
+  timeout 300 python scripts/prof_run.py $1 $2 > $OUT/plain_$1.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_propagate -s $(( $2 - 3 )) -c 1 \
+     -o $OUT/prop_$1 -f python scripts/prof_run.py $1 $2 > $OUT/ncu_prop_$1.log 2>&1
+done
+timeout 300 python scripts/prof_run.py forest_di6 40 > /dev/null 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_select -s 74 -c 2 \
+   -o $OUT/sel_forest_di6 -f python scripts/prof_run.py forest_di6 40 > $OUT/ncu_sel.log 2>&1
 echo done
