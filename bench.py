@@ -55,15 +55,19 @@ def _peaks():
     return p
 
 
-# Algorithmic FP32 lane-ops (FFMA/FADD/FMUL/FSETP/FMNMX/FDIV-as-1) of the
-# pinned recipe, per unit of device work counted by kp_profile.
-OPS_PER_STEP = {  # RK4 stages + combine + bounds/workspace compares + distance + cost add
-    "double_integrator_4d": 3 * 4 + 4 * 4 + 2 + (8 + 4) + 6 + 1,
-    "double_integrator_6d": 3 * 6 + 4 * 6 + 2 + (12 + 6) + 9 + 1,
-    "dubins_airplane_6d": 4 * (2 * 22 + 3) + 3 * 6 + 4 * 6 + 2 + 6 + (12 + 6) + 9 + 1,
-    "quadcopter_12d": 4 * (3 * 22 + 32) + 3 * 12 + 4 * 12 + 2 + 18 + (24 + 6) + 9 + 1,
+# Algorithmic FP32 lane-ops of the implemented recipe (FFMA, FADD, FMUL, FSETP,
+# FMNMX, FRND, FDIV, FSQRT each = 1), per unit of device work counted by
+# kp_profile.  Per RK4 step: 3N stage FMAs + 4N combine + 1 (h/2)
+# + 2N bound compares + distance (7 in 3-D, 5 in 2-D) + 1 cost add + 4
+# derivative evaluations (+2 per wrapped angle).  sincos recipe = 15.
+_SINCOS = 15
+OPS_PER_STEP = {
+    "double_integrator_4d": 3 * 4 + 4 * 4 + 1 + 8 + 5 + 1,                       # 43
+    "double_integrator_6d": 3 * 6 + 4 * 6 + 1 + 12 + 7 + 1,                      # 63
+    "dubins_airplane_6d": 3 * 6 + 4 * 6 + 1 + 12 + 7 + 1 + 2 + 4 * (2 * _SINCOS + 4),   # 201
+    "quadcopter_12d": 3 * 12 + 4 * 12 + 1 + 24 + 7 + 1 + 6 + 4 * (3 * _SINCOS + 26),   # 407
 }
-OPS_PER_ITEM = 30      # sampling (4 fma + 4 cvt/mul), S = ceil(dt/h), region index, goal test, acc add
+OPS_PER_ITEM = 35      # U conversions + control FMAs, S = ceil(dt/h), region index (3 dims), goal test, acc add
 OPS_PER_BOX = 6        # six closed-interval compares
 OPS_PER_SPHERE = 7     # 3 sub + mul + 2 fma + compare
 OPS_PER_INTERP = 4     # j/k + 3 fma
@@ -363,11 +367,20 @@ def roofline(scenario, pa, pb):
     t_sel = d["t_select_s"] / n_sel
     sel_gbs = sel_bytes / n_sel / t_sel / 1e9 if t_sel > 0 else 0.0
     t_total = d["t_propagate_s"] + d["t_select_s"] + d["t_scatter_s"]
+    traffic = None  # dram read+write bytes per launch from the committed ncu --set full capture
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        cfg_name = scenario.get("name", "")
+        kname = f"kp::k_propagate<{ {'double_integrator_4d': 0, 'double_integrator_6d': 1, 'dubins_airplane_6d': 2, 'quadcopter_12d': 3}[model] }>"
+        traffic = tr.get(cfg_name, {}).get(kname, {}).get("dram_bytes")
+    except Exception:
+        pass
     return {
         "kernel": "k_propagate",
         "bound": "fp32",
         "achieved": achieved / 1e12, "peak": pk["fp32_lane_ops"] / 1e12, "unit": "T lane-op/s",
-        "frac": achieved / pk["fp32_lane_ops"], "traffic": None,
+        "frac": achieved / pk["fp32_lane_ops"], "traffic": traffic,
+        "traffic_note": "dram bytes/launch of a steady-state launch, profiles/ncu_traffic.json (working set is L2-resident)",
         "peak_src": pk["fp32_src"],
         "ops_per_launch": ops_launch, "avg_launch_us": t_prop * 1e6, "launches": n_prop,
         "ops_convention": "FP32 lane-ops of the pinned recipe: FFMA, FADD, FMUL, FSETP, FMNMX, FDIV each = 1",

@@ -31,6 +31,7 @@
 // "last block" ticket pattern (threadfence + atomic counter), never a spin.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "kp_math.cuh"
 #include "kp_types.h"
@@ -42,6 +43,13 @@ KP_DEV unsigned long long globaltimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+
+// Programmatic dependent launch (sm_90+): a kernel may start while its
+// predecessor drains; griddepcontrol.wait blocks until the predecessor grid
+// has completed and its memory is visible, so nothing before it may read data
+// the predecessor writes.  launch_dependents lets the successor launch early.
+KP_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+KP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Stage the environment blob into shared memory (16-byte vector copies).
 KP_DEV Env stage_env(const KpProblem& P, const KpBuffers& B, float4* smem) {
@@ -81,6 +89,10 @@ __global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propa
     extern __shared__ float4 smem4[];
     __shared__ PropSmem<MODEL> sh;
     KpCtl* ctl = B.ctl;
+    if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
+    const Env E = stage_env(P, B, smem4);  // constant data: overlaps the predecessor's tail
+    pdl_wait();
+    pdl_trigger();
     if (ctl->done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
     const uint32_t n_items = ctl->n_items;
@@ -88,8 +100,6 @@ __global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propa
     const uint32_t CH = KP_PROP_THREADS * G;
     const uint32_t n_chunks = (n_items + CH - 1) / CH;
     if (blockIdx.x >= n_chunks) return;  // nothing for this block this iteration
-    if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
-    const Env E = stage_env(P, B, smem4);
     const uint32_t it = ctl->iter;
     const unsigned long long seed = ctl->seed;
     const uint32_t* __restrict__ va = B.va[it & 1];
@@ -303,9 +313,10 @@ KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, ui
 
 __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P, KpBuffers B) {
     KpCtl* ctl = B.ctl;
+    pdl_wait();
+    pdl_trigger();
     if (ctl->done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_sel_ns = globaltimer();
-    __shared__ unsigned int s_last;
     __shared__ uint32_t s_st[7];
     const uint32_t it = ctl->iter;
     const uint32_t n_live = ctl->n_live;
@@ -358,7 +369,6 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
     if (nlive) atomicAdd(&s_st[4], nlive);
     if (nslot) atomicAdd(&s_st[5], nslot);
     if (nadm) atomicAdd(&s_st[6], nadm);
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_st[0]) atomicAdd(&ctl->stats.pruned_terminal, static_cast<unsigned long long>(s_st[0]));
@@ -368,68 +378,63 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
         if (s_st[4]) atomicAdd(&ctl->stats.live_scanned, static_cast<unsigned long long>(s_st[4]));
         if (s_st[5]) atomicAdd(&ctl->stats.slots_scanned, static_cast<unsigned long long>(s_st[5]));
         if (s_st[6]) atomicAdd(&ctl->stats.admitted_checked, static_cast<unsigned long long>(s_st[6]));
-        __threadfence();
-        s_last = (atomicAdd(&ctl->ticket_a, 1u) == n_part - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // last block: exclusive scan of the tile counts.  Each thread owns a
-    // contiguous chunk of tiles: sequential sum, one block scan, sequential write.
-    const uint32_t chunk = (n_tiles + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
-    const uint32_t t0 = threadIdx.x * chunk;
-    const uint32_t t1 = min(t0 + chunk, n_tiles);
-    Cnt3 x{0, 0, 0};
-    for (uint32_t t = t0; t < t1; ++t) {
-        x.k += B.tile_sums[t];
-        x.v += B.tile_sums[B.max_tiles + t];
-        x.c += B.tile_sums[2 * B.max_tiles + t];
-    }
-    Cnt3 carry;
-    const Cnt3 inc = block_scan3(x, &carry);
-    Cnt3 run{inc.k - x.k, inc.v - x.v, inc.c - x.c};
-    for (uint32_t t = t0; t < t1; ++t) {
-        const uint32_t a = B.tile_sums[t], b = B.tile_sums[B.max_tiles + t], c = B.tile_sums[2 * B.max_tiles + t];
-        B.tile_prefix[t] = run.k;
-        B.tile_prefix[B.max_tiles + t] = run.v;
-        B.tile_prefix[2 * B.max_tiles + t] = run.c;
-        run.k += a; run.v += b; run.c += c;
-    }
-    if (threadIdx.x == 0) {
-        const uint32_t remaining = P.capacity - ctl->n_nodes;
-        ctl->n_tiles = n_tiles;
-        ctl->tot_keep = carry.k;
-        ctl->tot_va = carry.v;
-        ctl->tot_commit = carry.c;
-        ctl->accepted = carry.c < remaining ? carry.c : remaining;
-        ctl->ticket_a = 0;
-        ctl->t_sel_end_ns = globaltimer();
-        __threadfence();
     }
 }
 
 __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem P, KpBuffers B) {
     KpCtl* ctl = B.ctl;
+    pdl_wait();
+    pdl_trigger();
     if (ctl->done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_scat_ns = globaltimer();
     __shared__ unsigned int s_last;
+    __shared__ uint32_t s_red[6][KP_SELECT_THREADS / 32];
     const uint32_t it = ctl->iter;
     const uint32_t n_live = ctl->n_live;
     const uint32_t live_pad = (n_live + 31u) & ~31u;
     const uint32_t n_items = ctl->n_items;
     const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
-    const uint32_t n_tiles = ctl->n_tiles;
+    const uint32_t n_tiles = (E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
     const uint32_t n_part = min(gridDim.x, n_tiles);
     if (blockIdx.x >= n_part) return;
-    const uint32_t tot_keep = ctl->tot_keep, tot_va = ctl->tot_va, accepted = ctl->accepted;
+    // contiguous tile range of this block; exclusive prefix of its first tile
+    // and the grand totals from one pass over the per-tile counts
+    const uint32_t per = (n_tiles + n_part - 1) / n_part;
+    const uint32_t tb = blockIdx.x * per, te = min(tb + per, n_tiles);
+    uint32_t acc[6] = {0, 0, 0, 0, 0, 0};  // before tb: k, v, c; all: k, v, c
+    for (uint32_t t = threadIdx.x; t < n_tiles; t += KP_SELECT_THREADS) {
+        const uint32_t k = B.tile_sums[t], v = B.tile_sums[B.max_tiles + t], c = B.tile_sums[2 * B.max_tiles + t];
+        acc[3] += k; acc[4] += v; acc[5] += c;
+        if (t < tb) { acc[0] += k; acc[1] += v; acc[2] += c; }
+    }
+    {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_down_sync(0xFFFFFFFFu, acc[q], off);
+            if (lane == 0) s_red[q][warp] = acc[q];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            uint32_t v = 0;
+            for (int w = 0; w < KP_SELECT_THREADS / 32; ++w) v += s_red[q][w];
+            acc[q] = v;
+        }
+    }
+    const uint32_t tot_keep = acc[3], tot_va = acc[4], tot_commit = acc[5];
     const uint32_t n_nodes = ctl->n_nodes;
+    const uint32_t remaining = P.capacity - n_nodes;
+    const uint32_t accepted = tot_commit < remaining ? tot_commit : remaining;
+    Cnt3 run{acc[0], acc[1], acc[2]};
     const uint32_t cap = P.capacity, S = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
     const uint32_t* __restrict__ live = B.live[it & 1];
     const uint32_t* __restrict__ va = B.va[it & 1];
     uint32_t* __restrict__ live_n = B.live[(it + 1) & 1];
     uint32_t* __restrict__ va_n = B.va[(it + 1) & 1];
-    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (uint32_t tile = tb; tile < te; ++tile) {
         const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
         Cnt3 x{0, 0, 0};
         uint32_t g = 0, s = 0;
@@ -451,9 +456,12 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
         Cnt3 tot;
         const Cnt3 inc = block_scan3(x, &tot);  // (barrier: every lane has read its goal bit)
         if (e >= live_pad && e < E && (threadIdx.x & 31) == 0) B.goal_mask[(e - live_pad) >> 5] = 0u;
-        const uint32_t pk = B.tile_prefix[tile] + inc.k - x.k;
-        const uint32_t pv = B.tile_prefix[B.max_tiles + tile] + inc.v - x.v;
-        const uint32_t pc = B.tile_prefix[2 * B.max_tiles + tile] + inc.c - x.c;
+        const uint32_t pk = run.k + inc.k - x.k;
+        const uint32_t pv = run.v + inc.v - x.v;
+        const uint32_t pc = run.c + inc.c - x.c;
+        run.k += tot.k;
+        run.v += tot.v;
+        run.c += tot.c;
         if (is_live && x.k) {
             live_n[pk] = g;
             if (x.v) va_n[pv] = g;
@@ -489,51 +497,58 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     if (!s_last || threadIdx.x != 0) return;
     __threadfence();
     // ---- iteration boundary ----
+    // all control-block reads first (one batch of independent loads), then writes
     const unsigned long long now = globaltimer();
     const uint32_t it1 = it + 1;
-    ctl->stats.attempted += n_items;
-    ctl->stats.committed += accepted;
-    if (ctl->tot_commit > accepted) {
-        ctl->stats.dropped_capacity += ctl->tot_commit - accepted;
+    const unsigned long long best = ctl->best;
+    const uint32_t tl_len = ctl->timeline_len;
+    const unsigned long long prev = tl_len ? ctl->timeline[tl_len - 1].best : ~0ull;
+    const unsigned long long t_start = ctl->t_start_ns, first_ns = ctl->first_ns, deadline = ctl->deadline_ns;
+    const unsigned long long t_prop = ctl->t_prop_ns, t_sel = ctl->t_sel_ns, t_scat = ctl->t_scat_ns;
+    const uint32_t max_iter_abs = ctl->max_iter_abs, stop_first = ctl->stop_first;
+    const unsigned long long st_att = ctl->stats.attempted, st_com = ctl->stats.committed;
+    const unsigned long long st_drop = ctl->stats.dropped_capacity;
+    const uint32_t n_live1 = tot_keep + accepted, n_va1 = tot_va + accepted, n_nodes1 = n_nodes + accepted;
+    const unsigned long long items = static_cast<unsigned long long>(n_va1) * lam;
+    ctl->stats.attempted = st_att + n_items;
+    ctl->stats.committed = st_com + accepted;
+    if (tot_commit > accepted) {
+        ctl->stats.dropped_capacity = st_drop + (tot_commit - accepted);
         ctl->capacity_exhausted = 1;
     }
-    ctl->n_nodes = n_nodes + accepted;
-    ctl->n_live = tot_keep + accepted;
-    ctl->n_va = tot_va + accepted;
-    const unsigned long long items = static_cast<unsigned long long>(ctl->n_va) * lam;
+    ctl->n_nodes = n_nodes1;
+    ctl->n_live = n_live1;
+    ctl->n_va = n_va1;
     ctl->iter = it1;
     ctl->t_last_ns = now;
-    const unsigned long long best = ctl->best;
-    const unsigned long long prev = ctl->timeline_len ? ctl->timeline[ctl->timeline_len - 1].best : ~0ull;
     if (best < prev) {  // strict improvement at this iteration boundary (cost bits are the high word)
-        if (ctl->timeline_len < KP_TIMELINE_CAP) {
-            KpTimeline& t = ctl->timeline[ctl->timeline_len];
+        if (tl_len < KP_TIMELINE_CAP) {
+            KpTimeline& t = ctl->timeline[tl_len];
             t.iteration = it1;
-            t.t_ns = now - ctl->t_start_ns;
+            t.t_ns = now - t_start;
             t.best = best;
-            ctl->timeline_len += 1;
+            ctl->timeline_len = tl_len + 1;
         }
-        if (ctl->first_ns == 0) {
-            ctl->first_ns = now - ctl->t_start_ns;
+        if (first_ns == 0) {
+            ctl->first_ns = now - t_start;
             ctl->first_iter = it1;
         }
-        ctl->best_ns = now - ctl->t_start_ns;
+        ctl->best_ns = now - t_start;
         ctl->best_iter = it1;
     }
     {
         KpTraceRec& tr = B.trace[it % KP_TRACE_CAP];
-        tr.t_ns = now - ctl->t_start_ns;
+        tr.t_ns = now - t_start;
         tr.iteration = it1;
         tr.items = n_items;
-        tr.live = ctl->n_live;
-        tr.frontier = ctl->n_va;
-        tr.nodes = ctl->n_nodes;
+        tr.live = n_live1;
+        tr.frontier = n_va1;
+        tr.nodes = n_nodes1;
         tr.committed = accepted;
-        const unsigned long long t0 = ctl->t_start_ns;
-        tr.t_prop = static_cast<uint32_t>(ctl->t_prop_ns - t0);
-        tr.t_sel = static_cast<uint32_t>(ctl->t_sel_ns - t0);
-        tr.t_sel_end = static_cast<uint32_t>(ctl->t_sel_end_ns - t0);
-        tr.t_scat = static_cast<uint32_t>(ctl->t_scat_ns - t0);
+        tr.t_prop = static_cast<uint32_t>(t_prop - t_start);
+        tr.t_sel = static_cast<uint32_t>(t_sel - t_start);
+        tr.t_sel_end = static_cast<uint32_t>(t_scat - t_start);
+        tr.t_scat = static_cast<uint32_t>(t_scat - t_start);
     }
     bool done = false;
     if (items > S) {
@@ -543,10 +558,10 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     } else {
         ctl->n_items = static_cast<uint32_t>(items);
     }
-    if (ctl->max_iter_abs && it1 >= ctl->max_iter_abs) done = true;
-    if (ctl->deadline_ns && now >= ctl->deadline_ns) done = true;
-    if (ctl->stop_first && best != ~0ull) done = true;
-    if (ctl->n_live == 0) done = true;
+    if (max_iter_abs && it1 >= max_iter_abs) done = true;
+    if (deadline && now >= deadline) done = true;
+    if (stop_first && best != ~0ull) done = true;
+    if (n_live1 == 0) done = true;
     ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
     if (done) {
@@ -706,20 +721,49 @@ namespace kp {
 
 size_t propagate_smem(const KpProblem& P) { return P.env_bytes; }
 
+static bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KP_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename Kern>
+static cudaError_t launch_k(Kern kernel, int grid, int block, size_t smem, cudaStream_t st, const KpProblem& P,
+                            const KpBuffers& B) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, P, B);
+}
+
 cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_prop, int grid_sel, cudaStream_t st,
                              int which) {
     const size_t smem = propagate_smem(P);
+    cudaError_t e = cudaSuccess;
     if (which & 1) {
         switch (P.model) {
-                case 0: k_propagate<0><<<grid_prop, KP_PROP_THREADS, smem, st>>>(P, B); break;
-            case 1: k_propagate<1><<<grid_prop, KP_PROP_THREADS, smem, st>>>(P, B); break;
-            case 2: k_propagate<2><<<grid_prop, KP_PROP_THREADS, smem, st>>>(P, B); break;
-            default: k_propagate<3><<<grid_prop, KP_PROP_THREADS, smem, st>>>(P, B); break;
+            case 0: e = launch_k(k_propagate<0>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
+            case 1: e = launch_k(k_propagate<1>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
+            case 2: e = launch_k(k_propagate<2>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
+            default: e = launch_k(k_propagate<3>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
         }
+        if (e != cudaSuccess) return e;
     }
-    if (which & 2) k_select_reduce<<<grid_sel, KP_SELECT_THREADS, 0, st>>>(P, B);
-    if (which & 4) k_select_scatter<<<grid_sel, KP_SELECT_THREADS, 0, st>>>(P, B);
-    return cudaGetLastError();
+    if (which & 2) {
+        e = launch_k(k_select_reduce, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
+        if (e != cudaSuccess) return e;
+    }
+    if (which & 4) e = launch_k(k_select_scatter, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
+    return e;
 }
 
 cudaError_t set_propagate_smem(const KpProblem& P) {

@@ -1,0 +1,29 @@
+"""The C++ drop-in API (include/kinoplan_b200/kinoplan.hpp): compiles and links
+against the library on CPU; runs on the GPU (-m gpu)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _build(tmp_path):
+    exe = str(tmp_path / "dropin")
+    lib = os.path.join(ROOT, "paper_2602_02846_b200", "lib")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "dropin_example.cpp"), "-L", lib, "-lkinoplan_b200",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    return exe
+
+
+def test_cpp_dropin_compiles_and_links(tmp_path):
+    assert os.path.exists(_build(tmp_path))
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_runs(tmp_path):
+    out = subprocess.run([_build(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, (out.returncode, out.stdout, out.stderr)
+    found, cost, iters, tcost, nsamp = out.stdout.split()
+    assert found == "1" and float(cost) > 12.0 and int(iters) > 10 and float(tcost) == float(cost)

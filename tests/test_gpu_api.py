@@ -1,0 +1,71 @@
+"""Solution output (§8f #1) and API behaviour on the GPU."""
+import math
+
+import numpy as np
+import pytest
+
+import kpo
+from paper_2602_02846_b200 import Planner, plan, scenarios
+from paper_2602_02846_b200.planner import InvalidProblemError
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("scene", ["forest_di6", "narrow_dubins6", "building_quad12", "zigzag2d"])
+def test_path_and_reintegrated_trajectory(scene):
+    s = scenarios.load(scene, stop_at_first_solution=True)
+    with Planner(s, seed=3) as g:
+        r = g.solve(budget_s=2.0)
+        assert r["found"]
+        p = g.path()
+        nodes = g.nodes()
+        k = len(p["acc"])
+        assert p["acc"][0] == 0.0 and np.all(np.diff(p["acc"]) > 0)  # monotone
+        assert np.float32(p["acc"][-1]) == np.float32(r["best_cost"])
+        # chain follows parent links and carries the stored node records
+        leaf = r["best_leaf"]
+        chain = [leaf]
+        while nodes["parent"][chain[-1]] >= 0:
+            chain.append(int(nodes["parent"][chain[-1]]))
+        chain = chain[::-1]
+        assert len(chain) == k
+        np.testing.assert_array_equal(p["states"], nodes["state"][chain].astype(np.float64))
+        t = g.trajectory()
+        # fp32 running sum of re-integrated segment costs == stored acc, bit-exact
+        run = np.float32(0.0)
+        for c in t["segment_costs"]:
+            run = np.float32(run + np.float32(c))
+        assert run == np.float32(r["best_cost"])
+        # every node state appears as the last sample of its segment
+        n_samp = t["samples"].shape[0]
+        assert n_samp > k
+        np.testing.assert_array_equal(t["samples"][0], p["states"][0])
+        np.testing.assert_array_equal(t["samples"][-1], p["states"][-1])
+        # the re-integrated samples are valid states of the problem (oracle checker)
+        o = kpo.Oracle(s, kpo.MIRROR32)
+        assert o.is_segment_valid(t["samples"])
+
+
+def test_plan_entry_point_and_errors():
+    s = scenarios.load("forest_di6")
+    r = plan(s, seed=9, budget_s=0.05)
+    assert r["found"] and r["path"]["states"].shape[1] == 6 and len(r["timeline"]) >= 1
+    tl = r["timeline"]
+    assert all(a["cost"] > b["cost"] for a, b in zip(tl, tl[1:]))
+    bad = scenarios.load("forest_di6")
+    ob = bad["problem"]["environment"]["obstacles"][0]
+    with Planner(bad) as g:
+        with pytest.raises(InvalidProblemError):
+            g.reset(1, x_init=[(ob["min"][0] + ob["max"][0]) / 2, (ob["min"][1] + ob["max"][1]) / 2, 5, 0, 0, 0])
+
+
+def test_budget_respected_and_trace():
+    s = scenarios.load("forest_di6")
+    with Planner(s, seed=2) as g:
+        r = g.solve(budget_s=0.02)
+        assert 0.02 <= r["elapsed_s"] < 0.025  # stops at the first boundary past the budget
+        tr = g.trace()
+        assert len(tr) == r["iterations"] and np.all(np.diff(tr["t_ns"].astype(np.int64)) > 0)
+        assert int(tr["items"].sum()) == r["propagations_attempted"]
+        prof = g.profile()
+        assert prof["items"] == r["propagations_attempted"] and prof["rk4_steps"] > prof["items"]
