@@ -395,6 +395,47 @@ def roofline(scenario, pa, pb):
     }
 
 
+def run_sweep(args, scenario):
+    """BASELINE config 5: propagate throughput vs samples per iteration
+    (2^14 .. 2^22) on a synthetic frontier, lambda = 32, M = 2^k / 32 nodes."""
+    import torch
+
+    from paper_2602_02846_b200 import Planner
+
+    pk = _peaks()
+    model = scenario["problem"]["model"]
+    s = json.loads(json.dumps(scenario))
+    s["planner"]["capacity"] = max(int(s["planner"].get("capacity", 0)), (1 << 22) // 32)
+    s["planner"]["max_slots"] = 1 << 22
+    rows = []
+    with ClockSampler(0) as clk, Planner(s, device=0, seed=1) as g:
+        g.sweep(1 << 10, launches=3)  # warm-up
+        for k in range(14, 23):
+            n = (1 << k) // int(s["planner"]["lambda"])
+            ms, one = g.sweep(n, launches=max(3, args.steps))
+            ops = (one["rk4_steps"] * OPS_PER_STEP[model] + one["items"] * OPS_PER_ITEM
+                   + one["box_tests"] * OPS_PER_BOX + one["sphere_tests"] * OPS_PER_SPHERE
+                   + one["interp_points"] * OPS_PER_INTERP)
+            rate = ops / (ms * 1e-3)
+            rows.append({"k": k, "items": one["items"], "frontier_nodes": n, "ms_per_launch": ms,
+                         "items_per_s": one["items"] / (ms * 1e-3), "rk4_steps": one["rk4_steps"],
+                         "lane_ops_per_launch": ops, "achieved_T_lane_ops": rate / 1e12,
+                         "frac": rate / pk["fp32_lane_ops"]})
+    best = max(rows, key=lambda r: r["frac"])
+    line = {"metric": "node propagations/sec (propagate kernel, synthetic frontier sweep)",
+            "value": best["items_per_s"], "unit": "propagations/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": 1, "higher_is_better": True, "dtype": "f32", "data": "synthetic frontier (positions uniform "
+            "in free space, hover-ish), region table reset per launch",
+            "config": {"workload": f"{args.config} propagate sweep 2^14..2^22 samples per launch", "lambda":
+                       s["planner"]["lambda"]},
+            "roofline": {"kernel": f"k_propagate<{model}>", "bound": "fp32", "achieved": best["achieved_T_lane_ops"],
+                         "peak": pk["fp32_lane_ops"] / 1e12, "unit": "T lane-op/s", "frac": best["frac"],
+                         "peak_src": pk["fp32_src"], "at_k": best["k"]},
+            "sweep": rows, "clocks": clk.summary()}
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -409,12 +450,15 @@ def main():
     ap.add_argument("--seed-base", type=int, default=1000)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="BASELINE config 5: propagate throughput sweep")
     args = ap.parse_args()
     from paper_2602_02846_b200 import scenarios
 
     scenario = scenarios.load(args.config)
     if args.impl == "reference":
         return run_reference(args, scenario)
+    if args.sweep:
+        return run_sweep(args, scenario)
     return run_b200(args, scenario)
 
 

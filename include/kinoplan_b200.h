@@ -286,6 +286,21 @@ int kp_get_trace(kp_planner* planner, kp_trace_entry* buf, size_t cap, size_t* l
  * so a caller can bracket work with its own CUDA events. */
 int kp_get_stream(kp_planner* planner, void** stream);
 
+/* ---- propagation sweep (BASELINE config 5) -------------------------------- */
+
+/* Replace the tree by a synthetic frontier of n_nodes valid states: positions
+ * uniform in the workspace (seeded, rejection-sampled against the obstacles),
+ * every other coordinate as x_init ("hover-ish"), all Active, so that one propagate launch processes
+ * n_nodes * lambda work items.  Needs capacity >= n_nodes and max_slots >=
+ * n_nodes * lambda.  The planner must be kp_reset before a normal solve. */
+int kp_sweep_setup(kp_planner* planner, uint64_t n_nodes, uint64_t seed);
+
+/* Launch the propagate kernel alone `launches` times on the synthetic frontier
+ * (region table reset to +inf before each launch, so every launch does the
+ * same work) and return the mean device time per launch (CUDA events) and
+ * the work counters of one launch. */
+int kp_sweep_run(kp_planner* planner, uint32_t launches, double* ms_per_launch, kp_profile* one_launch);
+
 /* ---- batched independent queries (BASELINE config 4) -------- */
 
 /* Solve K independent seeded queries of the same problem on one device, one

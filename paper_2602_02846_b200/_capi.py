@@ -315,6 +315,10 @@ def load_library() -> C.CDLL:
     L.kp_get_trace.restype = I
     L.kp_get_stream.argtypes = [P, CP(C.c_void_p)]
     L.kp_get_stream.restype = I
+    L.kp_sweep_setup.argtypes = [P, C.c_uint64, C.c_uint64]
+    L.kp_sweep_setup.restype = I
+    L.kp_sweep_run.argtypes = [P, C.c_uint32, CP(D), CP(Profile)]
+    L.kp_sweep_run.restype = I
     L.kp_abi_version.argtypes = []
     L.kp_abi_version.restype = I
     _LIB = L
@@ -325,7 +329,7 @@ EXPORTED_SYMBOLS = [
     "kp_create", "kp_destroy", "kp_last_error", "kp_reset", "kp_reset_query", "kp_set_stop_at_first_solution",
     "kp_solve", "kp_get_timeline", "kp_get_path",
     "kp_get_trajectory", "kp_get_nodes", "kp_get_region_table", "kp_get_grid", "kp_debug_propagate",
-    "kp_set_profiling", "kp_get_profile", "kp_get_trace", "kp_get_stream", "kp_solve_batch", "kp_abi_version",
+    "kp_set_profiling", "kp_get_profile", "kp_get_trace", "kp_get_stream", "kp_solve_batch", "kp_sweep_setup", "kp_sweep_run", "kp_abi_version",
 ]
 
 

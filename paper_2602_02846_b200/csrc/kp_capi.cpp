@@ -42,6 +42,7 @@ cudaError_t launch_debug_propagate(const KpProblem& P, const KpBuffers& B, uint3
                                    uint32_t* steps, uint8_t* goals, cudaStream_t st);
 cudaError_t launch_chain(const KpBuffers& B, int32_t leaf, int32_t* chain, uint32_t cap, uint32_t* len,
                          cudaStream_t st);
+cudaError_t launch_sweep_prepare(const KpProblem& P, const KpBuffers& B, uint32_t n, cudaStream_t st);
 cudaError_t launch_gather_chain(const KpProblem& P, const KpBuffers& B, const int32_t* chain, uint32_t len,
                                 float* st, float* ct, float* dts, float* accs, cudaStream_t s);
 cudaError_t launch_reintegrate(const KpProblem& P, const KpBuffers& B, const int32_t* chain, uint32_t n_seg,
@@ -85,6 +86,7 @@ struct kp_planner {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     uint64_t seed = 0;
     uint64_t kernel_launches = 0, graph_launches = 0;
+    uint32_t sweep_nodes = 0;
     std::vector<float> boxes, spheres;  // host copies for start-state validation
     float* h_x0 = nullptr;              // pinned staging for the query's start state
 
@@ -431,6 +433,7 @@ void capture_graph(kp_planner* pl) {
 
 void do_reset(kp_planner* pl, uint64_t seed) {
     pl->seed = seed;
+    pl->sweep_nodes = 0;
     cuda_check(cudaMemcpyAsync(pl->B.x0, pl->h_x0, sizeof(float) * KP_MAX_N, cudaMemcpyHostToDevice, pl->stream),
                "x0 H2D");
     cuda_check(kp::launch_reset(pl->P, pl->B, seed, pl->stream), "reset");
@@ -775,6 +778,82 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
         if (pl->ctl.error == 8)
             throw KpError(KP_ERR_SLOT_OVERFLOW, "lambda*|V_A| exceeded max_slots; raise kp_config_desc.max_slots");
         fill_result(pl, out);
+    });
+}
+
+int kp_sweep_setup(kp_planner* pl, uint64_t n_nodes, uint64_t seed) {
+    if (!pl) return KP_ERR_ARGUMENT;
+    return guard(pl, [&] {
+        const KpProblem& P = pl->P;
+        if (n_nodes < 1 || n_nodes > P.capacity) throw KpError(KP_ERR_CONFIG, "sweep: n_nodes must be in [1, capacity]");
+        if (n_nodes * static_cast<uint64_t>(P.lambda) > P.max_slots)
+            throw KpError(KP_ERR_CONFIG, "sweep: n_nodes * lambda exceeds max_slots");
+        cuda_check(cudaSetDevice(pl->device), "cudaSetDevice");
+        // synthetic frontier: uniform in the (folded) bounds, rejection against the environment
+        uint64_t st = seed ? seed : 0x9E3779B97F4A7C15ULL;
+        auto next = [&] {
+            st += 0x9E3779B97F4A7C15ULL;
+            uint64_t z = st;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+            return z ^ (z >> 31);
+        };
+        std::vector<float> soa(static_cast<size_t>(P.n) * n_nodes);
+        KpProblem q = P;
+        for (uint64_t i = 0; i < n_nodes; ++i) {
+            for (int tries = 0;; ++tries) {
+                for (int d = 0; d < P.n; ++d) {  // positions uniform in free space, the rest as x_init (hover-ish)
+                    if (d >= P.ws_dim) { q.x_init[d] = P.x_init[d]; continue; }
+                    const double u = static_cast<double>(next() >> 11) * 0x1.0p-53;
+                    const float lo = P.blo[d], hi = P.bhi[d];
+                    q.x_init[d] = lo + static_cast<float>(u) * (hi - lo);
+                }
+                if (host_state_valid(q, pl->boxes, pl->spheres)) break;
+                if (tries > 100000) throw KpError(KP_ERR_INVALID_PROBLEM, "sweep: could not sample valid states");
+            }
+            for (int d = 0; d < P.n; ++d) soa[static_cast<size_t>(d) * n_nodes + i] = q.x_init[d];
+        }
+        for (int d = 0; d < P.n; ++d)
+            cuda_check(cudaMemcpyAsync(pl->B.state + static_cast<size_t>(d) * P.capacity, soa.data() + d * n_nodes,
+                                       n_nodes * 4, cudaMemcpyHostToDevice, pl->stream), "sweep H2D");
+        cuda_check(cudaMemsetAsync(pl->B.acc, 0, n_nodes * 4, pl->stream), "sweep acc");
+        pl->sweep_nodes = static_cast<uint32_t>(n_nodes);
+        cuda_check(cudaStreamSynchronize(pl->stream), "sweep sync");
+        pl->ctl_valid = false;
+    });
+}
+
+int kp_sweep_run(kp_planner* pl, uint32_t launches, double* ms_per_launch, kp_profile* one) {
+    if (!pl || !ms_per_launch) return KP_ERR_ARGUMENT;
+    return guard(pl, [&] {
+        if (!pl->sweep_nodes) throw KpError(KP_ERR_CONFIG, "sweep: call kp_sweep_setup first");
+        cuda_check(cudaSetDevice(pl->device), "cudaSetDevice");
+        double total = 0;
+        for (uint32_t k = 0; k < std::max(1u, launches); ++k) {
+            cuda_check(kp::launch_sweep_prepare(pl->P, pl->B, pl->sweep_nodes, pl->stream), "sweep prepare");
+            cuda_check(cudaEventRecord(pl->ev[0], pl->stream), "event");
+            cuda_check(kp::launch_iteration(pl->P, pl->B, pl->grid_prop, pl->grid_sel, pl->stream, 1), "sweep launch");
+            cuda_check(cudaEventRecord(pl->ev[1], pl->stream), "event");
+            cuda_check(cudaEventSynchronize(pl->ev[1]), "event sync");
+            float ms = 0;
+            cuda_check(cudaEventElapsedTime(&ms, pl->ev[0], pl->ev[1]), "elapsed");
+            total += ms;
+            pl->kernel_launches += 2;
+        }
+        *ms_per_launch = total / std::max(1u, launches);
+        if (one) {
+            fetch_ctl(pl);
+            const KpStats& st = pl->ctl.stats;
+            std::memset(one, 0, sizeof *one);
+            one->items = pl->ctl.n_items;
+            one->rk4_steps = st.rk4_steps;
+            one->samples_checked = st.rk4_steps;
+            one->interp_points = st.interp_points;
+            one->box_tests = st.box_tests;
+            one->sphere_tests = st.sphere_tests;
+            one->n_propagate = 1;
+            one->t_propagate_s = *ms_per_launch * 1e-3;
+        }
     });
 }
 

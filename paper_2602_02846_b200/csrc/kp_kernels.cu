@@ -821,6 +821,32 @@ cudaError_t launch_debug_propagate(const KpProblem& P, const KpBuffers& B, uint3
     return cudaGetLastError();
 }
 
+// Sweep support: frontier = nodes 0..n-1, iteration counter fixed, region
+// table +inf, counters cleared (one launch = n * lambda work items).
+__global__ void k_sweep_prepare(KpProblem P, KpBuffers B, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint32_t r = i; r < P.n_regions; r += gridDim.x * blockDim.x) B.rc[r] = 0x7F800000u;
+    for (uint32_t k = i; k < n; k += gridDim.x * blockDim.x) B.va[0][k] = k;
+    for (uint32_t w = i; w < P.max_slots / 32; w += gridDim.x * blockDim.x) {
+        B.admit_mask[w] = 0u;
+        B.goal_mask[w] = 0u;
+    }
+    if (i == 0) {
+        KpCtl* c = B.ctl;
+        c->done = 0;
+        c->iter = 0;
+        c->n_va = n;
+        c->n_items = n * static_cast<uint32_t>(P.lambda);
+        c->prop_cursor = 0;
+        c->stats = KpStats{};
+    }
+}
+
+cudaError_t launch_sweep_prepare(const KpProblem& P, const KpBuffers& B, uint32_t n, cudaStream_t st) {
+    k_sweep_prepare<<<148 * 4, 256, 0, st>>>(P, B, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_chain(const KpBuffers& B, int32_t leaf, int32_t* chain, uint32_t cap, uint32_t* len,
                          cudaStream_t st) {
     k_chain<<<1, 32, 0, st>>>(B, leaf, chain, cap, len);

@@ -212,6 +212,16 @@ class Planner:
                        ("t_prop", np.uint32), ("t_sel", np.uint32), ("t_sel_end", np.uint32), ("t_scat", np.uint32)])
         return np.frombuffer(bytes(buf)[: n.value * dt.itemsize], dtype=dt).copy()
 
+    def sweep(self, n_nodes: int, launches: int = 5, seed: int = 1) -> tuple[float, dict]:
+        """Propagate-kernel throughput on a synthetic frontier of n_nodes
+        (n_nodes * lambda items per launch; BASELINE config 5).  Returns
+        (ms per launch, work counters of one launch)."""
+        self._check(self._lib.kp_sweep_setup(self._h, n_nodes, seed))
+        ms = C.c_double()
+        pr = _capi.Profile()
+        self._check(self._lib.kp_sweep_run(self._h, launches, C.byref(ms), C.byref(pr)))
+        return ms.value, pr.as_dict()
+
     def stream(self) -> int:
         s = C.c_void_p()
         self._check(self._lib.kp_get_stream(self._h, C.byref(s)))
