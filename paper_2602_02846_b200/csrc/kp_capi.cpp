@@ -320,8 +320,8 @@ bool host_state_valid(const KpProblem& P, const std::vector<float>& boxes, const
 }
 
 // Environment blob: obstacles as float4 + an exact broad-phase cell grid over
-// the workspace.  Cells per dim ~ workspace extent / median obstacle extent
-// (<= 32), shrunk until <= 8192 cells and <= 65535 list entries; every
+// the workspace.  Cells per dim ~ 2 x workspace extent / median obstacle extent
+// (<= 64), shrunk until <= 16384 cells and < 32768 list entries; every
 // obstacle is listed in every cell its AABB (expanded by a margin of 1e-3
 // cell, far above the fp32 error of the device's cell computation) touches.
 std::vector<uint8_t> build_env(KpProblem& P, const std::vector<float>& boxes, const std::vector<float>& spheres) {
@@ -351,7 +351,9 @@ std::vector<uint8_t> build_env(KpProblem& P, const std::vector<float>& boxes, co
             std::nth_element(sz.begin(), sz.begin() + sz.size() / 2, sz.end());
             med = sz[sz.size() / 2];
         }
-        n[d] = std::max(1, std::min(32, static_cast<int>(std::lround(ext / med))));
+        // cells about half the median obstacle extent: most cells list 0-1 candidates,
+        // which keeps the lanes of a warp on the same narrow-phase trip count
+        n[d] = std::max(1, std::min(64, static_cast<int>(std::lround(2.0 * ext / med))));
         if (no == 0 || !(ext > 0)) n[d] = 1;
     }
     std::vector<std::vector<uint16_t>> lists;
@@ -377,7 +379,7 @@ std::vector<uint8_t> build_env(KpProblem& P, const std::vector<float>& boxes, co
                         ++entries;
                     }
         }
-        if ((nc <= 8192 && entries < 65535) || nc == 1) {
+        if ((nc <= 16384 && entries < 32768) || nc == 1) {
             if (entries >= 65535) throw KpError(KP_ERR_SCHEMA, "too many obstacle cell entries");
             break;
         }
