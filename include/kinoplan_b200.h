@@ -304,10 +304,23 @@ int kp_sweep_run(kp_planner* planner, uint32_t launches, double* ms_per_launch, 
 /* ---- batched independent queries (BASELINE config 4) -------- */
 
 /* Solve K independent seeded queries of the same problem on one device, one
- * query after another on the handle's stream (replicas-only semantics, no
- * cross-query interaction).  results[K]. */
+ * query after another on the handle's stream.  results[K]. */
 int kp_solve_batch(kp_planner* planner, const uint64_t* seeds, size_t k, double budget_s,
                    uint64_t max_iterations, kp_result* results);
+
+/* Concurrent batch engine: `lanes` independent planner instances (own device
+ * buffers, stream and CUDA graph each) on one device, fed by one asynchronous
+ * host scheduler, so the kernels of different queries overlap on the GPU.
+ * Queries share nothing (replicas-only semantics). */
+typedef struct kp_batch kp_batch;
+int kp_batch_create(const kp_problem_desc* problem, const kp_config_desc* config, int device, int lanes,
+                    kp_batch** out);
+void kp_batch_destroy(kp_batch* batch);
+const char* kp_batch_last_error(const kp_batch* batch);
+/* Solve queries seeds[0..k) (each with budget_s / max_iterations as
+ * kp_solve); results[k] in seed order; *wall_s = host wall time of the batch. */
+int kp_batch_solve(kp_batch* batch, const uint64_t* seeds, size_t k, double budget_s, uint64_t max_iterations,
+                   kp_result* results, double* wall_s);
 
 int kp_abi_version(void);
 

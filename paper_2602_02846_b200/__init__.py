@@ -5,6 +5,7 @@ holds the ctypes mirror of that ABI, the Python mirror of the reference API and
 the bundled scenario files."""
 from . import scenarios  # noqa: F401
 from .planner import (  # noqa: F401
+    BatchPlanner,
     ConfigError,
     DeviceError,
     GridTooFineError,
@@ -15,5 +16,5 @@ from .planner import (  # noqa: F401
     plan,
 )
 
-__all__ = ["Planner", "plan", "scenarios", "SchemaError", "InvalidProblemError", "ConfigError",
+__all__ = ["Planner", "BatchPlanner", "plan", "scenarios", "SchemaError", "InvalidProblemError", "ConfigError",
            "GridTooFineError", "InvalidSegmentError", "DeviceError"]

@@ -319,6 +319,14 @@ def load_library() -> C.CDLL:
     L.kp_sweep_setup.restype = I
     L.kp_sweep_run.argtypes = [P, C.c_uint32, CP(D), CP(Profile)]
     L.kp_sweep_run.restype = I
+    L.kp_batch_create.argtypes = [CP(ProblemDesc), CP(ConfigDesc), I, I, CP(P)]
+    L.kp_batch_create.restype = I
+    L.kp_batch_destroy.argtypes = [P]
+    L.kp_batch_destroy.restype = None
+    L.kp_batch_last_error.argtypes = [P]
+    L.kp_batch_last_error.restype = C.c_char_p
+    L.kp_batch_solve.argtypes = [P, CP(C.c_uint64), C.c_size_t, D, C.c_uint64, CP(Result), CP(D)]
+    L.kp_batch_solve.restype = I
     L.kp_abi_version.argtypes = []
     L.kp_abi_version.restype = I
     _LIB = L
@@ -329,7 +337,8 @@ EXPORTED_SYMBOLS = [
     "kp_create", "kp_destroy", "kp_last_error", "kp_reset", "kp_reset_query", "kp_set_stop_at_first_solution",
     "kp_solve", "kp_get_timeline", "kp_get_path",
     "kp_get_trajectory", "kp_get_nodes", "kp_get_region_table", "kp_get_grid", "kp_debug_propagate",
-    "kp_set_profiling", "kp_get_profile", "kp_get_trace", "kp_get_stream", "kp_solve_batch", "kp_sweep_setup", "kp_sweep_run", "kp_abi_version",
+    "kp_set_profiling", "kp_get_profile", "kp_get_trace", "kp_get_stream", "kp_solve_batch", "kp_sweep_setup", "kp_sweep_run", "kp_batch_create", "kp_batch_destroy",
+    "kp_batch_last_error", "kp_batch_solve", "kp_abi_version",
 ]
 
 

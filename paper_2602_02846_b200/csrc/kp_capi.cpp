@@ -89,6 +89,7 @@ struct kp_planner {
     uint32_t sweep_nodes = 0;
     std::vector<float> boxes, spheres;  // host copies for start-state validation
     float* h_x0 = nullptr;              // pinned staging for the query's start state
+    KpCtl* h_ctl = nullptr;             // pinned copy target for asynchronous result fetches
 
     template <class T>
     T* dalloc(size_t count) {
@@ -105,6 +106,7 @@ struct kp_planner {
         for (void* p : allocs) cudaFree(p);
         if (host_done) cudaFreeHost(host_done);
         if (h_x0) cudaFreeHost(h_x0);
+        if (h_ctl) cudaFreeHost(h_ctl);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -433,15 +435,19 @@ void capture_graph(kp_planner* pl) {
     cudaGraphDestroy(g);
 }
 
-void do_reset(kp_planner* pl, uint64_t seed) {
+void reset_async(kp_planner* pl, uint64_t seed) {
     pl->seed = seed;
     pl->sweep_nodes = 0;
     cuda_check(cudaMemcpyAsync(pl->B.x0, pl->h_x0, sizeof(float) * KP_MAX_N, cudaMemcpyHostToDevice, pl->stream),
                "x0 H2D");
     cuda_check(kp::launch_reset(pl->P, pl->B, seed, pl->stream), "reset");
     pl->kernel_launches += 2;
-    cuda_check(cudaStreamSynchronize(pl->stream), "reset sync");
     pl->ctl_valid = false;
+}
+
+void do_reset(kp_planner* pl, uint64_t seed) {
+    reset_async(pl, seed);
+    cuda_check(cudaStreamSynchronize(pl->stream), "reset sync");
 }
 
 void fetch_ctl(kp_planner* pl) {
@@ -608,6 +614,9 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         for (int i = 0; i < KP_MAX_N; ++i) pl->h_x0[i] = i < P.n ? P.x_init[i] : 0.0f;
         pl->boxes = boxes;
         pl->spheres = spheres;
+        void* hc = nullptr;
+        cuda_check(cudaHostAlloc(&hc, sizeof(KpCtl), cudaHostAllocDefault), "cudaHostAlloc ctl");
+        pl->h_ctl = static_cast<KpCtl*>(hc);
         cuda_check(kp::set_propagate_smem(P), "smem attribute");
         const int occ = std::max(1, kp::propagate_occupancy(P));
         pl->grid_prop = pl->sms * occ;
@@ -869,6 +878,120 @@ int kp_solve_batch(kp_planner* pl, const uint64_t* seeds, size_t k, double budge
         if (rc) return rc;
     }
     return KP_OK;
+}
+
+}  // extern "C"
+
+struct kp_batch {
+    std::vector<kp_planner*> lanes;
+    std::string err;
+    ~kp_batch() {
+        for (auto* l : lanes) delete l;
+    }
+};
+
+extern "C" {
+
+int kp_batch_create(const kp_problem_desc* problem, const kp_config_desc* config, int device, int lanes,
+                    kp_batch** out) {
+    if (!out || lanes < 1 || lanes > 256) return KP_ERR_ARGUMENT;
+    *out = nullptr;
+    auto* b = new kp_batch();
+    for (int i = 0; i < lanes; ++i) {
+        kp_planner* pl = nullptr;
+        const int rc = kp_create(problem, config, device, &pl);
+        if (rc != KP_OK) {
+            delete b;
+            return rc;  // message in kp_last_error(NULL)
+        }
+        b->lanes.push_back(pl);
+    }
+    *out = b;
+    return KP_OK;
+}
+
+void kp_batch_destroy(kp_batch* b) { delete b; }
+
+const char* kp_batch_last_error(const kp_batch* b) { return b ? b->err.c_str() : ""; }
+
+int kp_batch_solve(kp_batch* b, const uint64_t* seeds, size_t k, double budget_s, uint64_t max_iterations,
+                   kp_result* results, double* wall_s) {
+    if (!b || (k && (!seeds || !results))) return KP_ERR_ARGUMENT;
+    try {
+        kp_planner* l0 = b->lanes[0];
+        cuda_check(cudaSetDevice(l0->device), "cudaSetDevice");
+        const double budget = budget_s >= 0 ? budget_s : l0->cfg.t_max_s;
+        const uint64_t mi = max_iterations ? max_iterations : l0->cfg.max_iterations;
+        const bool stop_first = l0->cfg.stop_at_first_solution != 0;
+        if (!(budget > 0) && mi == 0 && !stop_first) throw KpError(KP_ERR_CONFIG, "batch solve needs a budget");
+        const unsigned long long budget_ns = budget > 0 ? static_cast<unsigned long long>(budget * 1e9) : 0ull;
+        enum State { IDLE, RUNNING, FETCHING };
+        struct LaneState {
+            State st = IDLE;
+            size_t q = 0;
+            int launched = 0;
+        };
+        std::vector<LaneState> ls(b->lanes.size());
+        size_t next = 0, finished = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto wall = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+        const double watchdog = (budget > 0 ? budget : 540.0) * (1.0 + static_cast<double>(k)) + 120.0;
+        while (finished < k) {
+            for (size_t i = 0; i < b->lanes.size(); ++i) {
+                kp_planner* pl = b->lanes[i];
+                LaneState& L = ls[i];
+                if (L.st == IDLE) {
+                    if (next >= k) continue;
+                    L.q = next++;
+                    reset_async(pl, seeds[L.q]);
+                    *pl->host_done = 0;
+                    cuda_check(kp::launch_start(pl->B, budget_ns, static_cast<uint32_t>(mi), stop_first ? 1u : 0u,
+                                                pl->stream), "start");
+                    pl->kernel_launches += 1;
+                    L.launched = 0;
+                    L.st = RUNNING;
+                }
+                if (L.st == RUNNING) {
+                    if (*pl->host_done) {
+                        cuda_check(cudaMemcpyAsync(pl->h_ctl, pl->B.ctl, sizeof(KpCtl), cudaMemcpyDeviceToHost,
+                                                   pl->stream), "ctl D2H");
+                        cuda_check(cudaEventRecord(pl->ev[0], pl->stream), "event");
+                        L.st = FETCHING;
+                    } else {
+                        cudaEvent_t e = pl->ev[2 + (L.launched & 1)];
+                        const bool slot_free = L.launched < 2 || cudaEventQuery(e) == cudaSuccess;
+                        if (slot_free) {
+                            cuda_check(cudaGraphLaunch(pl->graph, pl->stream), "cudaGraphLaunch");
+                            cuda_check(cudaEventRecord(e, pl->stream), "event");
+                            pl->graph_launches += 1;
+                            pl->kernel_launches += 3 * KP_GRAPH_ITERS;
+                            ++L.launched;
+                        }
+                    }
+                }
+                if (L.st == FETCHING) {
+                    const cudaError_t q = cudaEventQuery(pl->ev[0]);
+                    if (q == cudaErrorNotReady) continue;
+                    cuda_check(q, "batch fetch");
+                    std::memcpy(&pl->ctl, pl->h_ctl, sizeof(KpCtl));
+                    pl->ctl_valid = true;
+                    if (pl->ctl.error == 8) throw KpError(KP_ERR_SLOT_OVERFLOW, "lambda*|V_A| exceeded max_slots");
+                    fill_result(pl, &results[L.q]);
+                    L.st = IDLE;
+                    ++finished;
+                }
+            }
+            if (wall() > watchdog) throw KpError(KP_ERR_CUDA, "batch watchdog expired");
+        }
+        if (wall_s) *wall_s = wall();
+        return KP_OK;
+    } catch (const KpError& e) {
+        b->err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        b->err = e.what();
+        return KP_ERR_ARGUMENT;
+    }
 }
 
 int kp_get_timeline(kp_planner* pl, kp_timeline_entry* buf, size_t cap, size_t* len) {

@@ -228,6 +228,49 @@ class Planner:
         return s.value or 0
 
 
+class BatchPlanner:
+    """Concurrent batch engine (BASELINE config 4): `lanes` planner instances
+    on one device, independent seeded queries overlapped on the GPU."""
+
+    def __init__(self, scenario: dict, lanes: int = 16, device: int = 0):
+        self._lib = load_library()
+        self.desc = Descriptors(scenario)
+        h = C.c_void_p()
+        rc = self._lib.kp_batch_create(C.byref(self.desc.problem), C.byref(self.desc.config), device, lanes,
+                                       C.byref(h))
+        if rc:
+            _raise(rc, self._lib.kp_last_error(None))
+        self._h = h
+        self.lanes = lanes
+
+    def solve(self, seeds, budget_s: float = -1.0, max_iterations: int = 0):
+        seeds = list(seeds)
+        arr = (C.c_uint64 * max(1, len(seeds)))(*seeds)
+        res = (Result * max(1, len(seeds)))()
+        wall = C.c_double()
+        rc = self._lib.kp_batch_solve(self._h, arr, len(seeds), budget_s, max_iterations, res, C.byref(wall))
+        if rc:
+            _raise(rc, self._lib.kp_batch_last_error(self._h))
+        return [r.as_dict() for r in res[: len(seeds)]], wall.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.kp_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 def plan(scenario: dict, seed: int | None = None, device: int = 0, budget_s: float = -1.0,
          max_iterations: int = 0) -> dict:
     """plan(problem, config): one fresh run; returns the result

@@ -69,3 +69,22 @@ def test_budget_respected_and_trace():
         assert int(tr["items"].sum()) == r["propagations_attempted"]
         prof = g.profile()
         assert prof["items"] == r["propagations_attempted"] and prof["rk4_steps"] > prof["items"]
+
+
+def test_batch_engine_matches_single_planner():
+    """Concurrent lanes are independent replicas: with an iteration budget each
+    query's result is identical to the same seed solved alone."""
+    from paper_2602_02846_b200 import BatchPlanner
+
+    s = scenarios.load("forest_di6", capacity=1 << 18, max_slots=1 << 21)
+    seeds = [11, 12, 13, 14, 15, 16, 17]
+    with BatchPlanner(s, lanes=3) as b:
+        res, wall = b.solve(seeds, budget_s=0.0, max_iterations=12)
+    assert wall > 0 and len(res) == len(seeds)
+    with Planner(s) as g:
+        for sd, r in zip(seeds, res):
+            g.reset(sd)
+            one = g.solve(0.0, 12)
+            for k in ("best_cost", "best_leaf", "node_count", "propagations_attempted", "propagations_valid",
+                      "iterations", "nodes_pruned_terminal"):
+                assert r[k] == one[k], (sd, k, r[k], one[k])
