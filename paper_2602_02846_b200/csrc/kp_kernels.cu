@@ -381,6 +381,89 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
     }
 }
 
+// Close an iteration: counts, stats, best / timeline / TTFS
+// from %globaltimer, trace record, termination.  One thread of the last block.
+KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t it, uint32_t n_items,
+                               uint32_t tot_keep, uint32_t tot_va, uint32_t tot_commit, uint32_t n_nodes,
+                               uint32_t accepted) {
+    KpCtl* ctl = B.ctl;
+    const uint32_t S = P.max_slots;
+    const uint32_t lam = static_cast<uint32_t>(P.lambda);
+    // all control-block reads first (one batch of independent loads), then writes
+    const unsigned long long now = globaltimer();
+    const uint32_t it1 = it + 1;
+    const unsigned long long best = ctl->best;
+    const uint32_t tl_len = ctl->timeline_len;
+    const unsigned long long prev = tl_len ? ctl->timeline[tl_len - 1].best : ~0ull;
+    const unsigned long long t_start = ctl->t_start_ns, first_ns = ctl->first_ns, deadline = ctl->deadline_ns;
+    const unsigned long long t_prop = ctl->t_prop_ns, t_sel = ctl->t_sel_ns, t_scat = ctl->t_scat_ns;
+    const uint32_t max_iter_abs = ctl->max_iter_abs, stop_first = ctl->stop_first;
+    const unsigned long long st_att = ctl->stats.attempted, st_com = ctl->stats.committed;
+    const unsigned long long st_drop = ctl->stats.dropped_capacity;
+    const uint32_t n_live1 = tot_keep + accepted, n_va1 = tot_va + accepted, n_nodes1 = n_nodes + accepted;
+    const unsigned long long items = static_cast<unsigned long long>(n_va1) * lam;
+    ctl->stats.attempted = st_att + n_items;
+    ctl->stats.committed = st_com + accepted;
+    if (tot_commit > accepted) {
+        ctl->stats.dropped_capacity = st_drop + (tot_commit - accepted);
+        ctl->capacity_exhausted = 1;
+    }
+    ctl->n_nodes = n_nodes1;
+    ctl->n_live = n_live1;
+    ctl->n_va = n_va1;
+    ctl->iter = it1;
+    ctl->t_last_ns = now;
+    if (best < prev) {  // strict improvement at this iteration boundary (cost bits are the high word)
+        if (tl_len < KP_TIMELINE_CAP) {
+            KpTimeline& t = ctl->timeline[tl_len];
+            t.iteration = it1;
+            t.t_ns = now - t_start;
+            t.best = best;
+            ctl->timeline_len = tl_len + 1;
+        }
+        if (first_ns == 0) {
+            ctl->first_ns = now - t_start;
+            ctl->first_iter = it1;
+        }
+        ctl->best_ns = now - t_start;
+        ctl->best_iter = it1;
+    }
+    {
+        KpTraceRec& tr = B.trace[it % KP_TRACE_CAP];
+        tr.t_ns = now - t_start;
+        tr.iteration = it1;
+        tr.items = n_items;
+        tr.live = n_live1;
+        tr.frontier = n_va1;
+        tr.nodes = n_nodes1;
+        tr.committed = accepted;
+        tr.t_prop = static_cast<uint32_t>(t_prop - t_start);
+        tr.t_sel = static_cast<uint32_t>(t_sel - t_start);
+        tr.t_sel_end = static_cast<uint32_t>(t_scat - t_start);
+        tr.t_scat = static_cast<uint32_t>(t_scat - t_start);
+    }
+    bool done = false;
+    if (items > S) {
+        ctl->error = 8;  // KP_ERR_SLOT_OVERFLOW
+        done = true;
+        ctl->n_items = 0;
+    } else {
+        ctl->n_items = static_cast<uint32_t>(items);
+    }
+    if (max_iter_abs && it1 >= max_iter_abs) done = true;
+    if (deadline && now >= deadline) done = true;
+    if (stop_first && best != ~0ull) done = true;
+    if (n_live1 == 0) done = true;
+    ctl->ticket_b = 0;
+    ctl->prop_cursor = 0;
+    ctl->sel_cursor = 0;
+    if (done) {
+        ctl->done = 1;
+        __threadfence_system();
+        *B.host_done = 1;
+    }
+}
+
 __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem P, KpBuffers B) {
     KpCtl* ctl = B.ctl;
     pdl_wait();
@@ -496,79 +579,222 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     __syncthreads();
     if (!s_last || threadIdx.x != 0) return;
     __threadfence();
-    // ---- iteration boundary ----
-    // all control-block reads first (one batch of independent loads), then writes
-    const unsigned long long now = globaltimer();
-    const uint32_t it1 = it + 1;
-    const unsigned long long best = ctl->best;
-    const uint32_t tl_len = ctl->timeline_len;
-    const unsigned long long prev = tl_len ? ctl->timeline[tl_len - 1].best : ~0ull;
-    const unsigned long long t_start = ctl->t_start_ns, first_ns = ctl->first_ns, deadline = ctl->deadline_ns;
-    const unsigned long long t_prop = ctl->t_prop_ns, t_sel = ctl->t_sel_ns, t_scat = ctl->t_scat_ns;
-    const uint32_t max_iter_abs = ctl->max_iter_abs, stop_first = ctl->stop_first;
-    const unsigned long long st_att = ctl->stats.attempted, st_com = ctl->stats.committed;
-    const unsigned long long st_drop = ctl->stats.dropped_capacity;
-    const uint32_t n_live1 = tot_keep + accepted, n_va1 = tot_va + accepted, n_nodes1 = n_nodes + accepted;
-    const unsigned long long items = static_cast<unsigned long long>(n_va1) * lam;
-    ctl->stats.attempted = st_att + n_items;
-    ctl->stats.committed = st_com + accepted;
-    if (tot_commit > accepted) {
-        ctl->stats.dropped_capacity = st_drop + (tot_commit - accepted);
-        ctl->capacity_exhausted = 1;
-    }
-    ctl->n_nodes = n_nodes1;
-    ctl->n_live = n_live1;
-    ctl->n_va = n_va1;
-    ctl->iter = it1;
-    ctl->t_last_ns = now;
-    if (best < prev) {  // strict improvement at this iteration boundary (cost bits are the high word)
-        if (tl_len < KP_TIMELINE_CAP) {
-            KpTimeline& t = ctl->timeline[tl_len];
-            t.iteration = it1;
-            t.t_ns = now - t_start;
-            t.best = best;
-            ctl->timeline_len = tl_len + 1;
+    iteration_boundary(P, B, it, n_items, tot_keep, tot_va, tot_commit, n_nodes, accepted);
+}
+
+// Fused select (prune + commit + compaction + scatter + iteration boundary) in
+// ONE pass: tiles of 256 elements are claimed in order by an atomic cursor;
+// each tile publishes its aggregate, obtains its exclusive prefix by a
+// warp-parallel decoupled look-back over its predecessors (which are held by
+// running blocks, so the look-back always completes), publishes its
+// inclusive prefix and scatters.  Counts per element: k = survivor (live) or
+// commit (slot), v = Active (live) or commit (slot), c = commit (slot): with
+// every live element ahead of every slot element, the running prefix puts a
+// new node right after all survivors without knowing their total.  Spins are
+// bounded by a %globaltimer watchdog (ctl->error = 9) so a bug cannot hang the GPU.
+#define KP_WATCHDOG_NS 200000000ull
+
+KP_DEV bool lb_wait(const volatile uint32_t* ea, const volatile uint32_t* ep, uint32_t epoch,
+                    unsigned long long deadline, KpCtl* ctl) {
+    // returns true when the prefix is published, false when only the aggregate is
+    for (;;) {
+        if (*ep == epoch) return true;
+        if (*ea == epoch) return false;
+        if (globaltimer() > deadline) {
+            ctl->error = 9;
+            return true;
         }
-        if (first_ns == 0) {
-            ctl->first_ns = now - t_start;
-            ctl->first_iter = it1;
+    }
+}
+
+__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select(KpProblem P, KpBuffers B) {
+    KpCtl* ctl = B.ctl;
+    pdl_wait();
+    pdl_trigger();
+    if (ctl->done) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_sel_ns = globaltimer();
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_excl[3];
+    __shared__ uint32_t s_st[7];
+    __shared__ unsigned int s_last;
+    const uint32_t it = ctl->iter;
+    const uint32_t epoch = it + 1;
+    const uint32_t n_live = ctl->n_live;
+    const uint32_t live_pad = (n_live + 31u) & ~31u;
+    const uint32_t n_items = ctl->n_items;
+    const uint32_t n_nodes = ctl->n_nodes;
+    const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
+    const uint32_t n_tiles = (E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
+    const uint32_t n_part = min(gridDim.x, n_tiles);
+    if (blockIdx.x >= n_part) return;
+    const unsigned long long deadline = globaltimer() + KP_WATCHDOG_NS;
+    const uint32_t remaining = P.capacity - n_nodes;
+    const uint32_t cap = P.capacity, S = P.max_slots;
+    const uint32_t lam = static_cast<uint32_t>(P.lambda);
+    const uint32_t MT = B.max_tiles;
+    const uint32_t* __restrict__ live = B.live[it & 1];
+    const uint32_t* __restrict__ va = B.va[it & 1];
+    uint32_t* __restrict__ live_n = B.live[(it + 1) & 1];
+    uint32_t* __restrict__ va_n = B.va[(it + 1) & 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t term = 0, deact = 0, react = 0, hops = 0, nlive = 0, nslot = 0, nadm = 0;
+    if (threadIdx.x < 7) s_st[threadIdx.x] = 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->sel_cursor, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= n_tiles) break;
+        const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
+        // ---- flags (prune / commit test) ----
+        Cnt3 x{0, 0, 0};
+        bool commit = false, is_live = false, is_slot = false;
+        uint32_t g = 0, sl = 0;
+        uint8_t st = KP_ST_TERMINAL;
+        if (e < n_live) {
+            is_live = true;
+            ++nlive;
+            g = live[e];
+            st = prune_node(P, B, g, &term, &deact, &react, &hops);
+            x.k = st != KP_ST_TERMINAL;
+            x.v = st == KP_ST_ACTIVE;
+        } else if (e >= live_pad && e < E) {
+            sl = e - live_pad;
+            if (sl < n_items) {
+                is_slot = true;
+                ++nslot;
+                if ((B.admit_mask[sl >> 5] >> (sl & 31)) & 1u) {
+                    ++nadm;
+                    commit = B.vu_acc[sl] == B.rc[B.vu_region[sl]];  // Alg. 4 line 3, bit-exact
+                    x.k = x.v = x.c = commit;
+                }
+            }
         }
-        ctl->best_ns = now - t_start;
-        ctl->best_iter = it1;
+        const uint32_t cm = __ballot_sync(0xFFFFFFFFu, commit);
+        const bool goal = commit && ((B.goal_mask[sl >> 5] >> (sl & 31)) & 1u);
+        __syncwarp();  // every lane has read its admit / goal bit before lane 0 clears the words
+        if (e >= live_pad && e < E && lane == 0) {
+            const uint32_t w = (e - live_pad) >> 5;
+            B.commit_mask[w] = cm;
+            B.admit_mask[w] = 0u;  // consumed
+            B.goal_mask[w] = 0u;
+        }
+        Cnt3 tot;
+        const Cnt3 inc = block_scan3(x, &tot);
+        // ---- publish aggregate, look back, publish inclusive prefix ----
+        if (threadIdx.x == 0) {
+            __stcg(B.tile_sums + tile, tot.k);
+            __stcg(B.tile_sums + MT + tile, tot.v);
+            __stcg(B.tile_sums + 2 * MT + tile, tot.c);
+            __threadfence();
+            *reinterpret_cast<volatile uint32_t*>(B.tile_epoch + tile) = epoch;
+        }
+        if (warp == 0) {
+            uint32_t ek = 0, ev = 0, ec = 0;
+            int32_t base = static_cast<int32_t>(tile);
+            while (base > 0) {
+                const int32_t j = base - 1 - lane;
+                bool isP = true;
+                if (j >= 0)
+                    isP = lb_wait(reinterpret_cast<volatile uint32_t*>(B.tile_epoch + j),
+                                  reinterpret_cast<volatile uint32_t*>(B.tile_epoch + MT + j), epoch, deadline, ctl);
+                __threadfence();
+                const uint32_t pm = __ballot_sync(0xFFFFFFFFu, isP);
+                const int pl = __ffs(pm) - 1;  // nearest predecessor with a published prefix (or virtual -1)
+                uint32_t a = 0, b = 0, c = 0;
+                if (pm == 0 || lane <= pl) {
+                    if (j >= 0) {
+                        const uint32_t* src = (pm != 0 && lane == pl) ? B.tile_prefix : B.tile_sums;
+                        a = __ldcg(src + j);
+                        b = __ldcg(src + MT + j);
+                        c = __ldcg(src + 2 * MT + j);
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    a += __shfl_down_sync(0xFFFFFFFFu, a, off);
+                    b += __shfl_down_sync(0xFFFFFFFFu, b, off);
+                    c += __shfl_down_sync(0xFFFFFFFFu, c, off);
+                }
+                a = __shfl_sync(0xFFFFFFFFu, a, 0);
+                b = __shfl_sync(0xFFFFFFFFu, b, 0);
+                c = __shfl_sync(0xFFFFFFFFu, c, 0);
+                ek += a; ev += b; ec += c;
+                if (pm != 0) break;
+                base -= 32;
+            }
+            if (lane == 0) {
+                s_excl[0] = ek; s_excl[1] = ev; s_excl[2] = ec;
+                __stcg(B.tile_prefix + tile, ek + tot.k);
+                __stcg(B.tile_prefix + MT + tile, ev + tot.v);
+                __stcg(B.tile_prefix + 2 * MT + tile, ec + tot.c);
+                __threadfence();
+                *reinterpret_cast<volatile uint32_t*>(B.tile_epoch + MT + tile) = epoch;
+            }
+        }
+        __syncthreads();
+        const uint32_t pk = s_excl[0] + inc.k - x.k;
+        const uint32_t pv = s_excl[1] + inc.v - x.v;
+        const uint32_t pc = s_excl[2] + inc.c - x.c;
+        // ---- scatter ----
+        if (is_live && x.k) {
+            live_n[pk] = g;
+            if (x.v) va_n[pv] = g;
+        }
+        if (is_slot && commit && pc < remaining) {
+            const uint32_t id = n_nodes + pc;
+#pragma unroll 4
+            for (int d = 0; d < P.n; ++d)
+                B.state[static_cast<size_t>(d) * cap + id] = B.vu_state[static_cast<size_t>(d) * S + sl];
+#pragma unroll 4
+            for (int d = 0; d < P.m; ++d)
+                B.ctrl[static_cast<size_t>(d) * cap + id] = B.vu_ctrl[static_cast<size_t>(d) * S + sl];
+            const uint32_t abits = B.vu_acc[sl];
+            const uint32_t par = va[sl / lam];
+            const uint32_t reg = B.vu_region[sl];
+            B.dt[id] = B.vu_dt[sl];
+            B.acc[id] = abits;
+            B.region[id] = reg;
+            B.parent[id] = static_cast<int32_t>(par);
+            B.link[id] = make_uint4(par, reg, abits, 0u);
+            B.status[id] = KP_ST_ACTIVE;
+            B.icnt[id] = 0;
+            live_n[pk] = id;  // == survivors + commit rank
+            va_n[pv] = id;
+            if (goal)  // Alg. 4 lines 5-7
+                atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
+        }
+        (void)is_slot;
+        __syncthreads();  // s_tile / s_excl reuse
     }
-    {
-        KpTraceRec& tr = B.trace[it % KP_TRACE_CAP];
-        tr.t_ns = now - t_start;
-        tr.iteration = it1;
-        tr.items = n_items;
-        tr.live = n_live1;
-        tr.frontier = n_va1;
-        tr.nodes = n_nodes1;
-        tr.committed = accepted;
-        tr.t_prop = static_cast<uint32_t>(t_prop - t_start);
-        tr.t_sel = static_cast<uint32_t>(t_sel - t_start);
-        tr.t_sel_end = static_cast<uint32_t>(t_scat - t_start);
-        tr.t_scat = static_cast<uint32_t>(t_scat - t_start);
+    // ---- stats, completion ticket, boundary ----
+    if (term) atomicAdd(&s_st[0], term);
+    if (deact) atomicAdd(&s_st[1], deact);
+    if (react) atomicAdd(&s_st[2], react);
+    if (hops) atomicAdd(&s_st[3], hops);
+    if (nlive) atomicAdd(&s_st[4], nlive);
+    if (nslot) atomicAdd(&s_st[5], nslot);
+    if (nadm) atomicAdd(&s_st[6], nadm);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_st[0]) atomicAdd(&ctl->stats.pruned_terminal, static_cast<unsigned long long>(s_st[0]));
+        if (s_st[1]) atomicAdd(&ctl->stats.deactivated, static_cast<unsigned long long>(s_st[1]));
+        if (s_st[2]) atomicAdd(&ctl->stats.reactivated, static_cast<unsigned long long>(s_st[2]));
+        if (s_st[3]) atomicAdd(&ctl->stats.ancestor_hops, static_cast<unsigned long long>(s_st[3]));
+        if (s_st[4]) atomicAdd(&ctl->stats.live_scanned, static_cast<unsigned long long>(s_st[4]));
+        if (s_st[5]) atomicAdd(&ctl->stats.slots_scanned, static_cast<unsigned long long>(s_st[5]));
+        if (s_st[6]) atomicAdd(&ctl->stats.admitted_checked, static_cast<unsigned long long>(s_st[6]));
+        __threadfence();
+        s_last = (atomicAdd(&ctl->ticket_b, 1u) == n_part - 1);
     }
-    bool done = false;
-    if (items > S) {
-        ctl->error = 8;  // KP_ERR_SLOT_OVERFLOW
-        done = true;
-        ctl->n_items = 0;
-    } else {
-        ctl->n_items = static_cast<uint32_t>(items);
-    }
-    if (max_iter_abs && it1 >= max_iter_abs) done = true;
-    if (deadline && now >= deadline) done = true;
-    if (stop_first && best != ~0ull) done = true;
-    if (n_live1 == 0) done = true;
-    ctl->ticket_b = 0;
-    ctl->prop_cursor = 0;
-    if (done) {
-        ctl->done = 1;
-        __threadfence_system();
-        *B.host_done = 1;
-    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    const uint32_t last = n_tiles - 1;
+    const uint32_t tk = __ldcg(B.tile_prefix + last), tv = __ldcg(B.tile_prefix + MT + last);
+    const uint32_t tc = __ldcg(B.tile_prefix + 2 * MT + last);
+    const uint32_t accepted = tc < remaining ? tc : remaining;
+    iteration_boundary(P, B, it, n_items, tk - tc, tv - tc, tc, n_nodes, accepted);
 }
 
 // Reset the region table and plant the root (Alg. 1 lines 1-5).
@@ -617,6 +843,7 @@ __global__ void k_start(KpBuffers B, unsigned long long budget_ns, uint32_t max_
     ctl->ticket_a = 0;
     ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
+    ctl->sel_cursor = 0;
     bool done = ctl->error != 0 || ctl->n_live == 0 || (stop_first && ctl->best != ~0ull);
     ctl->done = done ? 1u : 0u;
     __threadfence_system();
@@ -729,6 +956,14 @@ static bool pdl_enabled() {
     return on;
 }
 
+bool fused_select() {
+    static const bool on = [] {
+        const char* e = std::getenv("KP_FUSED_SELECT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <typename Kern>
 static cudaError_t launch_k(Kern kernel, int grid, int block, size_t smem, cudaStream_t st, const KpProblem& P,
                             const KpBuffers& B) {
@@ -757,6 +992,10 @@ cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_pr
             default: e = launch_k(k_propagate<3>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
         }
         if (e != cudaSuccess) return e;
+    }
+    if (fused_select()) {  // one pass: prune + commit + compaction + scatter + boundary
+        if (which & 2) e = launch_k(k_select, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
+        return e;
     }
     if (which & 2) {
         e = launch_k(k_select_reduce, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
@@ -793,6 +1032,7 @@ int propagate_occupancy(const KpProblem& P) {
 cudaError_t launch_reset(const KpProblem& P, const KpBuffers& B, unsigned long long seed, cudaStream_t st) {
     cudaMemsetAsync(B.ctl, 0, sizeof(KpCtl), st);
     cudaMemsetAsync(B.admit_mask, 0, sizeof(uint32_t) * (P.max_slots / 32), st);
+    cudaMemsetAsync(B.tile_epoch, 0, sizeof(uint32_t) * 2 * B.max_tiles, st);
     cudaMemsetAsync(B.goal_mask, 0, sizeof(uint32_t) * (P.max_slots / 32), st);
     k_reset_table<<<148 * 4, 256, 0, st>>>(P, B);
     k_reset_root<<<1, 32, 0, st>>>(P, B, seed);
