@@ -584,28 +584,14 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
 
 // Fused select (prune + commit + compaction + scatter + iteration boundary) in
 // ONE pass: tiles of 256 elements are claimed in order by an atomic cursor;
-// each tile publishes its aggregate, obtains its exclusive prefix by a
-// warp-parallel decoupled look-back over its predecessors (which are held by
-// running blocks, so the look-back always completes), publishes its
-// inclusive prefix and scatters.  Counts per element: k = survivor (live) or
+// each tile publishes its aggregate, then sums the aggregates of all its
+// predecessors (claimed earlier by running blocks, so they always publish;
+// one warp loads them in parallel) and scatters.  Counts per element: k = survivor (live) or
 // commit (slot), v = Active (live) or commit (slot), c = commit (slot): with
 // every live element ahead of every slot element, the running prefix puts a
 // new node right after all survivors without knowing their total.  Spins are
 // bounded by a %globaltimer watchdog (ctl->error = 9) so a bug cannot hang the GPU.
 #define KP_WATCHDOG_NS 200000000ull
-
-KP_DEV bool lb_wait(const volatile uint32_t* ea, const volatile uint32_t* ep, uint32_t epoch,
-                    unsigned long long deadline, KpCtl* ctl) {
-    // returns true when the prefix is published, false when only the aggregate is
-    for (;;) {
-        if (*ep == epoch) return true;
-        if (*ea == epoch) return false;
-        if (globaltimer() > deadline) {
-            ctl->error = 9;
-            return true;
-        }
-    }
-}
 
 __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select(KpProblem P, KpBuffers B) {
     KpCtl* ctl = B.ctl;
@@ -689,46 +675,31 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select(KpProblem P, KpBuf
             *reinterpret_cast<volatile uint32_t*>(B.tile_epoch + tile) = epoch;
         }
         if (warp == 0) {
-            uint32_t ek = 0, ev = 0, ec = 0;
-            int32_t base = static_cast<int32_t>(tile);
-            while (base > 0) {
-                const int32_t j = base - 1 - lane;
-                bool isP = true;
-                if (j >= 0)
-                    isP = lb_wait(reinterpret_cast<volatile uint32_t*>(B.tile_epoch + j),
-                                  reinterpret_cast<volatile uint32_t*>(B.tile_epoch + MT + j), epoch, deadline, ctl);
-                __threadfence();
-                const uint32_t pm = __ballot_sync(0xFFFFFFFFu, isP);
-                const int pl = __ffs(pm) - 1;  // nearest predecessor with a published prefix (or virtual -1)
-                uint32_t a = 0, b = 0, c = 0;
-                if (pm == 0 || lane <= pl) {
-                    if (j >= 0) {
-                        const uint32_t* src = (pm != 0 && lane == pl) ? B.tile_prefix : B.tile_sums;
-                        a = __ldcg(src + j);
-                        b = __ldcg(src + MT + j);
-                        c = __ldcg(src + 2 * MT + j);
+            // exclusive prefix = sum of every predecessor's aggregate: all tiles are
+            // in flight together here, so waiting for published prefixes would chain;
+            // the lanes instead load all predecessor aggregates in parallel
+            uint32_t a = 0, b = 0, c = 0;
+            for (uint32_t j = lane; j < tile; j += 32) {
+                const volatile uint32_t* ej = reinterpret_cast<volatile uint32_t*>(B.tile_epoch + j);
+                while (*ej != epoch) {
+                    if (globaltimer() > deadline) {
+                        ctl->error = 9;
+                        break;
                     }
                 }
+                __threadfence();
+                a += __ldcg(B.tile_sums + j);
+                b += __ldcg(B.tile_sums + MT + j);
+                c += __ldcg(B.tile_sums + 2 * MT + j);
+            }
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    a += __shfl_down_sync(0xFFFFFFFFu, a, off);
-                    b += __shfl_down_sync(0xFFFFFFFFu, b, off);
-                    c += __shfl_down_sync(0xFFFFFFFFu, c, off);
-                }
-                a = __shfl_sync(0xFFFFFFFFu, a, 0);
-                b = __shfl_sync(0xFFFFFFFFu, b, 0);
-                c = __shfl_sync(0xFFFFFFFFu, c, 0);
-                ek += a; ev += b; ec += c;
-                if (pm != 0) break;
-                base -= 32;
+            for (int off = 16; off > 0; off >>= 1) {
+                a += __shfl_down_sync(0xFFFFFFFFu, a, off);
+                b += __shfl_down_sync(0xFFFFFFFFu, b, off);
+                c += __shfl_down_sync(0xFFFFFFFFu, c, off);
             }
             if (lane == 0) {
-                s_excl[0] = ek; s_excl[1] = ev; s_excl[2] = ec;
-                __stcg(B.tile_prefix + tile, ek + tot.k);
-                __stcg(B.tile_prefix + MT + tile, ev + tot.v);
-                __stcg(B.tile_prefix + 2 * MT + tile, ec + tot.c);
-                __threadfence();
-                *reinterpret_cast<volatile uint32_t*>(B.tile_epoch + MT + tile) = epoch;
+                s_excl[0] = a; s_excl[1] = b; s_excl[2] = c;
             }
         }
         __syncthreads();
@@ -788,11 +759,18 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select(KpProblem P, KpBuf
         s_last = (atomicAdd(&ctl->ticket_b, 1u) == n_part - 1);
     }
     __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
+    if (!s_last) return;
     __threadfence();
-    const uint32_t last = n_tiles - 1;
-    const uint32_t tk = __ldcg(B.tile_prefix + last), tv = __ldcg(B.tile_prefix + MT + last);
-    const uint32_t tc = __ldcg(B.tile_prefix + 2 * MT + last);
+    Cnt3 tsum{0, 0, 0};  // grand totals: sum of all tile aggregates (block-parallel)
+    for (uint32_t j = threadIdx.x; j < n_tiles; j += KP_SELECT_THREADS) {
+        tsum.k += __ldcg(B.tile_sums + j);
+        tsum.v += __ldcg(B.tile_sums + MT + j);
+        tsum.c += __ldcg(B.tile_sums + 2 * MT + j);
+    }
+    Cnt3 tall;
+    block_scan3(tsum, &tall);
+    if (threadIdx.x != 0) return;
+    const uint32_t tk = tall.k, tv = tall.v, tc = tall.c;
     const uint32_t accepted = tc < remaining ? tc : remaining;
     iteration_boundary(P, B, it, n_items, tk - tc, tv - tc, tc, n_nodes, accepted);
 }
