@@ -601,7 +601,6 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         B.max_tiles = static_cast<uint32_t>((max_e + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS);
         B.tile_sums = pl->dalloc<uint32_t>(3ull * B.max_tiles);
         B.tile_prefix = pl->dalloc<uint32_t>(3ull * B.max_tiles);
-        B.tile_epoch = pl->dalloc<uint32_t>(2ull * B.max_tiles);
         const std::vector<uint8_t> blob = build_env(pl->P, boxes, spheres);
         float4* denv = pl->dalloc<float4>(blob.size() / 16);
         cuda_check(cudaMemcpy(denv, blob.data(), blob.size(), cudaMemcpyHostToDevice), "env H2D");
@@ -787,7 +786,6 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
             }
         }
         fetch_ctl(pl);
-        if (pl->ctl.error == 9) throw KpError(KP_ERR_CUDA, "device watchdog: select look-back did not complete");
         if (pl->ctl.error == 8)
             throw KpError(KP_ERR_SLOT_OVERFLOW, "lambda*|V_A| exceeded max_slots; raise kp_config_desc.max_slots");
         fill_result(pl, out);

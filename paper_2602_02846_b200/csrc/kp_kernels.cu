@@ -456,7 +456,6 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
     if (n_live1 == 0) done = true;
     ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
-    ctl->sel_cursor = 0;
     if (done) {
         ctl->done = 1;
         __threadfence_system();
@@ -485,10 +484,23 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     const uint32_t per = (n_tiles + n_part - 1) / n_part;
     const uint32_t tb = blockIdx.x * per, te = min(tb + per, n_tiles);
     uint32_t acc[6] = {0, 0, 0, 0, 0, 0};  // before tb: k, v, c; all: k, v, c
-    for (uint32_t t = threadIdx.x; t < n_tiles; t += KP_SELECT_THREADS) {
-        const uint32_t k = B.tile_sums[t], v = B.tile_sums[B.max_tiles + t], c = B.tile_sums[2 * B.max_tiles + t];
-        acc[3] += k; acc[4] += v; acc[5] += c;
-        if (t < tb) { acc[0] += k; acc[1] += v; acc[2] += c; }
+    constexpr int U = 8;  // 8 independent loads per array in flight per thread
+    for (uint32_t base = threadIdx.x; base < n_tiles; base += U * KP_SELECT_THREADS) {
+        uint32_t kk[U], vv[U], cc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t t = base + u * KP_SELECT_THREADS;
+            const bool in = t < n_tiles;
+            kk[u] = in ? B.tile_sums[t] : 0u;
+            vv[u] = in ? B.tile_sums[B.max_tiles + t] : 0u;
+            cc[u] = in ? B.tile_sums[2 * B.max_tiles + t] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t t = base + u * KP_SELECT_THREADS;
+            acc[3] += kk[u]; acc[4] += vv[u]; acc[5] += cc[u];
+            if (t < tb) { acc[0] += kk[u]; acc[1] += vv[u]; acc[2] += cc[u]; }
+        }
     }
     {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -582,199 +594,6 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     iteration_boundary(P, B, it, n_items, tot_keep, tot_va, tot_commit, n_nodes, accepted);
 }
 
-// Fused select (prune + commit + compaction + scatter + iteration boundary) in
-// ONE pass: tiles of 256 elements are claimed in order by an atomic cursor;
-// each tile publishes its aggregate, then sums the aggregates of all its
-// predecessors (claimed earlier by running blocks, so they always publish;
-// one warp loads them in parallel) and scatters.  Counts per element: k = survivor (live) or
-// commit (slot), v = Active (live) or commit (slot), c = commit (slot): with
-// every live element ahead of every slot element, the running prefix puts a
-// new node right after all survivors without knowing their total.  Spins are
-// bounded by a %globaltimer watchdog (ctl->error = 9) so a bug cannot hang the GPU.
-#define KP_WATCHDOG_NS 200000000ull
-
-__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select(KpProblem P, KpBuffers B) {
-    KpCtl* ctl = B.ctl;
-    pdl_wait();
-    pdl_trigger();
-    if (ctl->done) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_sel_ns = globaltimer();
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_excl[3];
-    __shared__ uint32_t s_st[7];
-    __shared__ unsigned int s_last;
-    const uint32_t it = ctl->iter;
-    const uint32_t epoch = it + 1;
-    const uint32_t n_live = ctl->n_live;
-    const uint32_t live_pad = (n_live + 31u) & ~31u;
-    const uint32_t n_items = ctl->n_items;
-    const uint32_t n_nodes = ctl->n_nodes;
-    const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
-    const uint32_t n_tiles = (E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
-    const uint32_t n_part = min(gridDim.x, n_tiles);
-    if (blockIdx.x >= n_part) return;
-    const unsigned long long deadline = globaltimer() + KP_WATCHDOG_NS;
-    const uint32_t remaining = P.capacity - n_nodes;
-    const uint32_t cap = P.capacity, S = P.max_slots;
-    const uint32_t lam = static_cast<uint32_t>(P.lambda);
-    const uint32_t MT = B.max_tiles;
-    const uint32_t* __restrict__ live = B.live[it & 1];
-    const uint32_t* __restrict__ va = B.va[it & 1];
-    uint32_t* __restrict__ live_n = B.live[(it + 1) & 1];
-    uint32_t* __restrict__ va_n = B.va[(it + 1) & 1];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t term = 0, deact = 0, react = 0, hops = 0, nlive = 0, nslot = 0, nadm = 0;
-    if (threadIdx.x < 7) s_st[threadIdx.x] = 0;
-    for (;;) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->sel_cursor, 1u);
-        __syncthreads();
-        const uint32_t tile = s_tile;
-        if (tile >= n_tiles) break;
-        const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
-        // ---- flags (prune / commit test) ----
-        Cnt3 x{0, 0, 0};
-        bool commit = false, is_live = false, is_slot = false;
-        uint32_t g = 0, sl = 0;
-        uint8_t st = KP_ST_TERMINAL;
-        if (e < n_live) {
-            is_live = true;
-            ++nlive;
-            g = live[e];
-            st = prune_node(P, B, g, &term, &deact, &react, &hops);
-            x.k = st != KP_ST_TERMINAL;
-            x.v = st == KP_ST_ACTIVE;
-        } else if (e >= live_pad && e < E) {
-            sl = e - live_pad;
-            if (sl < n_items) {
-                is_slot = true;
-                ++nslot;
-                if ((B.admit_mask[sl >> 5] >> (sl & 31)) & 1u) {
-                    ++nadm;
-                    commit = B.vu_acc[sl] == B.rc[B.vu_region[sl]];  // Alg. 4 line 3, bit-exact
-                    x.k = x.v = x.c = commit;
-                }
-            }
-        }
-        const uint32_t cm = __ballot_sync(0xFFFFFFFFu, commit);
-        const bool goal = commit && ((B.goal_mask[sl >> 5] >> (sl & 31)) & 1u);
-        __syncwarp();  // every lane has read its admit / goal bit before lane 0 clears the words
-        if (e >= live_pad && e < E && lane == 0) {
-            const uint32_t w = (e - live_pad) >> 5;
-            B.commit_mask[w] = cm;
-            B.admit_mask[w] = 0u;  // consumed
-            B.goal_mask[w] = 0u;
-        }
-        Cnt3 tot;
-        const Cnt3 inc = block_scan3(x, &tot);
-        // ---- publish aggregate, look back, publish inclusive prefix ----
-        if (threadIdx.x == 0) {
-            __stcg(B.tile_sums + tile, tot.k);
-            __stcg(B.tile_sums + MT + tile, tot.v);
-            __stcg(B.tile_sums + 2 * MT + tile, tot.c);
-            __threadfence();
-            *reinterpret_cast<volatile uint32_t*>(B.tile_epoch + tile) = epoch;
-        }
-        if (warp == 0) {
-            // exclusive prefix = sum of every predecessor's aggregate: all tiles are
-            // in flight together here, so waiting for published prefixes would chain;
-            // the lanes instead load all predecessor aggregates in parallel
-            uint32_t a = 0, b = 0, c = 0;
-            for (uint32_t j = lane; j < tile; j += 32) {
-                const volatile uint32_t* ej = reinterpret_cast<volatile uint32_t*>(B.tile_epoch + j);
-                while (*ej != epoch) {
-                    if (globaltimer() > deadline) {
-                        ctl->error = 9;
-                        break;
-                    }
-                }
-                __threadfence();
-                a += __ldcg(B.tile_sums + j);
-                b += __ldcg(B.tile_sums + MT + j);
-                c += __ldcg(B.tile_sums + 2 * MT + j);
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                a += __shfl_down_sync(0xFFFFFFFFu, a, off);
-                b += __shfl_down_sync(0xFFFFFFFFu, b, off);
-                c += __shfl_down_sync(0xFFFFFFFFu, c, off);
-            }
-            if (lane == 0) {
-                s_excl[0] = a; s_excl[1] = b; s_excl[2] = c;
-            }
-        }
-        __syncthreads();
-        const uint32_t pk = s_excl[0] + inc.k - x.k;
-        const uint32_t pv = s_excl[1] + inc.v - x.v;
-        const uint32_t pc = s_excl[2] + inc.c - x.c;
-        // ---- scatter ----
-        if (is_live && x.k) {
-            live_n[pk] = g;
-            if (x.v) va_n[pv] = g;
-        }
-        if (is_slot && commit && pc < remaining) {
-            const uint32_t id = n_nodes + pc;
-#pragma unroll 4
-            for (int d = 0; d < P.n; ++d)
-                B.state[static_cast<size_t>(d) * cap + id] = B.vu_state[static_cast<size_t>(d) * S + sl];
-#pragma unroll 4
-            for (int d = 0; d < P.m; ++d)
-                B.ctrl[static_cast<size_t>(d) * cap + id] = B.vu_ctrl[static_cast<size_t>(d) * S + sl];
-            const uint32_t abits = B.vu_acc[sl];
-            const uint32_t par = va[sl / lam];
-            const uint32_t reg = B.vu_region[sl];
-            B.dt[id] = B.vu_dt[sl];
-            B.acc[id] = abits;
-            B.region[id] = reg;
-            B.parent[id] = static_cast<int32_t>(par);
-            B.link[id] = make_uint4(par, reg, abits, 0u);
-            B.status[id] = KP_ST_ACTIVE;
-            B.icnt[id] = 0;
-            live_n[pk] = id;  // == survivors + commit rank
-            va_n[pv] = id;
-            if (goal)  // Alg. 4 lines 5-7
-                atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
-        }
-        (void)is_slot;
-        __syncthreads();  // s_tile / s_excl reuse
-    }
-    // ---- stats, completion ticket, boundary ----
-    if (term) atomicAdd(&s_st[0], term);
-    if (deact) atomicAdd(&s_st[1], deact);
-    if (react) atomicAdd(&s_st[2], react);
-    if (hops) atomicAdd(&s_st[3], hops);
-    if (nlive) atomicAdd(&s_st[4], nlive);
-    if (nslot) atomicAdd(&s_st[5], nslot);
-    if (nadm) atomicAdd(&s_st[6], nadm);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (s_st[0]) atomicAdd(&ctl->stats.pruned_terminal, static_cast<unsigned long long>(s_st[0]));
-        if (s_st[1]) atomicAdd(&ctl->stats.deactivated, static_cast<unsigned long long>(s_st[1]));
-        if (s_st[2]) atomicAdd(&ctl->stats.reactivated, static_cast<unsigned long long>(s_st[2]));
-        if (s_st[3]) atomicAdd(&ctl->stats.ancestor_hops, static_cast<unsigned long long>(s_st[3]));
-        if (s_st[4]) atomicAdd(&ctl->stats.live_scanned, static_cast<unsigned long long>(s_st[4]));
-        if (s_st[5]) atomicAdd(&ctl->stats.slots_scanned, static_cast<unsigned long long>(s_st[5]));
-        if (s_st[6]) atomicAdd(&ctl->stats.admitted_checked, static_cast<unsigned long long>(s_st[6]));
-        __threadfence();
-        s_last = (atomicAdd(&ctl->ticket_b, 1u) == n_part - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    Cnt3 tsum{0, 0, 0};  // grand totals: sum of all tile aggregates (block-parallel)
-    for (uint32_t j = threadIdx.x; j < n_tiles; j += KP_SELECT_THREADS) {
-        tsum.k += __ldcg(B.tile_sums + j);
-        tsum.v += __ldcg(B.tile_sums + MT + j);
-        tsum.c += __ldcg(B.tile_sums + 2 * MT + j);
-    }
-    Cnt3 tall;
-    block_scan3(tsum, &tall);
-    if (threadIdx.x != 0) return;
-    const uint32_t tk = tall.k, tv = tall.v, tc = tall.c;
-    const uint32_t accepted = tc < remaining ? tc : remaining;
-    iteration_boundary(P, B, it, n_items, tk - tc, tv - tc, tc, n_nodes, accepted);
-}
-
 // Reset the region table and plant the root (Alg. 1 lines 1-5).
 __global__ void k_reset_table(KpProblem P, KpBuffers B) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_regions; i += gridDim.x * blockDim.x)
@@ -821,7 +640,6 @@ __global__ void k_start(KpBuffers B, unsigned long long budget_ns, uint32_t max_
     ctl->ticket_a = 0;
     ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
-    ctl->sel_cursor = 0;
     bool done = ctl->error != 0 || ctl->n_live == 0 || (stop_first && ctl->best != ~0ull);
     ctl->done = done ? 1u : 0u;
     __threadfence_system();
@@ -934,14 +752,6 @@ static bool pdl_enabled() {
     return on;
 }
 
-bool fused_select() {
-    static const bool on = [] {
-        const char* e = std::getenv("KP_FUSED_SELECT");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 template <typename Kern>
 static cudaError_t launch_k(Kern kernel, int grid, int block, size_t smem, cudaStream_t st, const KpProblem& P,
                             const KpBuffers& B) {
@@ -970,10 +780,6 @@ cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_pr
             default: e = launch_k(k_propagate<3>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
         }
         if (e != cudaSuccess) return e;
-    }
-    if (fused_select()) {  // one pass: prune + commit + compaction + scatter + boundary
-        if (which & 2) e = launch_k(k_select, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
-        return e;
     }
     if (which & 2) {
         e = launch_k(k_select_reduce, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
@@ -1010,7 +816,6 @@ int propagate_occupancy(const KpProblem& P) {
 cudaError_t launch_reset(const KpProblem& P, const KpBuffers& B, unsigned long long seed, cudaStream_t st) {
     cudaMemsetAsync(B.ctl, 0, sizeof(KpCtl), st);
     cudaMemsetAsync(B.admit_mask, 0, sizeof(uint32_t) * (P.max_slots / 32), st);
-    cudaMemsetAsync(B.tile_epoch, 0, sizeof(uint32_t) * 2 * B.max_tiles, st);
     cudaMemsetAsync(B.goal_mask, 0, sizeof(uint32_t) * (P.max_slots / 32), st);
     k_reset_table<<<148 * 4, 256, 0, st>>>(P, B);
     k_reset_root<<<1, 32, 0, st>>>(P, B, seed);

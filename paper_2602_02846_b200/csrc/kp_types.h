@@ -103,7 +103,6 @@ struct KpCtl {
     uint32_t tot_keep, tot_va, tot_commit, accepted;
     uint32_t ticket_a, ticket_b;
     uint32_t prop_cursor;     // dynamic chunk cursor of k_propagate (reset at every boundary)
-    uint32_t sel_cursor;      // in-order tile cursor of the fused k_select (reset at every boundary)
     // run bookkeeping
     uint32_t max_iter_abs;    // stop when iter >= this (0 = unlimited)
     uint32_t stop_first;
@@ -145,9 +144,8 @@ struct KpBuffers {
     uint32_t* goal_mask;    // [max_slots/32]
     uint32_t* commit_mask;  // [max_slots/32]
     // select scratch
-    uint32_t* tile_sums;    // [3][max_tiles] per-tile aggregates (look-back)
-    uint32_t* tile_prefix;  // [3][max_tiles] per-tile inclusive prefixes (look-back)
-    uint32_t* tile_epoch;   // [2][max_tiles] iteration+1 at which aggregate / prefix were published
+    uint32_t* tile_sums;    // [3][max_tiles] per-tile counts (keep, active, commit)
+    uint32_t* tile_prefix;  // [3][max_tiles] (unused scratch)
     uint32_t max_tiles;
     const float4* env;      // environment blob (see KpProblem)
     KpTraceRec* trace;      // [KP_TRACE_CAP] ring, one record per iteration boundary
