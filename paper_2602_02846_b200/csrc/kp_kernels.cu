@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propa
             atomicOr(B.admit_mask + (i >> 5), 1u << (i & 31));
             if (o.goal) atomicOr(B.goal_mask + (i >> 5), 1u << (i & 31));
         }
+        if (n_chunks <= gridDim.x) break;  // every chunk was assigned statically
         __syncthreads();
         if (threadIdx.x == 0) sh.chunk = gridDim.x + atomicAdd(&ctl->prop_cursor, 1u);
         __syncthreads();
