@@ -359,10 +359,14 @@ KP_DEV int integrate_item(const KpProblem& P, const Env& E, float* x, const floa
     o.nsph = 0;
     const float h6 = P.h / 6.0f;
     for (int s = 0; s < S; ++s) {
-        const bool last = s + 1 >= S;
-        const float hk = last ? dt - static_cast<float>(S - 1) * P.h : P.h;
-        if (!(hk > 0.0f)) break;
-        if (!rk4_step<MODEL>(P, x, u, hk, last ? hk / 6.0f : h6)) return 2;
+        float hk = P.h, sixth = h6;
+        if (s + 1 == S) {  // the shortened last step: only here the IEEE division
+            hk = dt - static_cast<float>(S - 1) * P.h;
+            if (!(hk > 0.0f)) break;
+            // IEEE div.rn (== hk / 6.0f); volatile so it is not if-converted into every step
+            asm volatile("div.rn.f32 %0, %1, %2;" : "=f"(sixth) : "f"(hk), "f"(6.0f));
+        }
+        if (!rk4_step<MODEL>(P, x, u, hk, sixth)) return 2;
         o.steps += 1;
         const float nx = x[0], ny = x[1], nz = TWO_D ? 0.0f : x[2];
         if (!within_bounds<MODEL>(P, x)) return 1;
