@@ -330,9 +330,10 @@ void derivative(const ProblemDef& pd, const Consts<P>& k, const Vec<typename P::
             out[4] = a * P::madd(t1, sps, -(sph * cps));
             out[5] = P::madd(a, cph * cth, -k.grav);
             const R w = P::madd(x[10], sph, x[11] * cph);  // q sin(phi) + r cos(phi)
-            out[6] = P::madd(w, sth / cth, x[9]);
+            const R ic = R(1) / cth;                          // sec(theta)
+            out[6] = P::madd(w, sth * ic, x[9]);
             out[7] = P::madd(x[10], cph, -(x[11] * sph));
-            out[8] = w / cth;
+            out[8] = w * ic;
             out[9] = P::madd(k.cx, x[10] * x[11], u[1] * k.inv_ix);
             out[10] = P::madd(k.cy, x[9] * x[11], u[2] * k.inv_iy);
             out[11] = P::madd(k.cz, x[9] * x[10], u[3] * k.inv_iz);

@@ -99,8 +99,12 @@ KP_DEV void sample_item(const KpProblem& P, uint64_t seed, uint32_t it, uint32_t
 // ----------------------------------------------------------------- math ---
 // Pinned sincos recipe, identical to the oracle's.
 KP_DEV void sincos_recipe(float x, float& s_out, float& c_out) {
-    const float j = rintf(x * 0x1.45f306p-1f);
-    const int q = static_cast<int>(j);
+    // j = rint(x * 2/pi) with round-half-even via the 1.5 * 2^23 magic add (bit-identical
+    // to rintf for |x * 2/pi| < 2^22) and the quadrant from the sum's integer bits: no
+    // XU-pipe conversion instructions
+    const float t = x * 0x1.45f306p-1f + 12582912.0f;
+    const float j = t - 12582912.0f;
+    const int q = __float_as_int(t) - 0x4B400000;
     float r = fmaf(-j, 0x1.921fb4p+0f, x);
     r = fmaf(-j, 0x1.4442d2p-24f, r);
     const float r2 = r * r;
@@ -166,9 +170,10 @@ KP_DEV void derivative(const KpProblem& P, const float* x, const float* u, float
         f[4] = a * fmaf(t1, sps, -(sph * cps));
         f[5] = fmaf(a, cph * cth, -P.grav);
         const float w = fmaf(x[10], sph, x[11] * cph);
-        f[6] = fmaf(w, sth / cth, x[9]);
+        const float ic = 1.0f / cth;  // one IEEE division per evaluation (recipe)
+        f[6] = fmaf(w, sth * ic, x[9]);
         f[7] = fmaf(x[10], cph, -(x[11] * sph));
-        f[8] = w / cth;
+        f[8] = w * ic;
         f[9] = fmaf(P.cx, x[10] * x[11], u[1] * P.inv_ix);
         f[10] = fmaf(P.cy, x[9] * x[11], u[2] * P.inv_iy);
         f[11] = fmaf(P.cz, x[9] * x[10], u[3] * P.inv_iz);
@@ -242,7 +247,11 @@ KP_DEV Env env_view(const KpProblem& P, const float4* base) {
 
 KP_DEV int bg_cell(const KpProblem& P, float v, int d) {
     if (P.bg_n[d] == 1) return 0;  // uniform branch: undivided dimension
-    int c = __float2int_rd((v - P.bg_lo[d]) * P.bg_inv[d]);
+    // floor(t) as rint(t - 0.5) with the magic add (no XU conversion): exact except at
+    // t == integer, where it may return the lower neighbour; obstacles touching a cell
+    // boundary are binned into both cells (margin), so the broad phase stays exact
+    const float t = fmaf(v - P.bg_lo[d], P.bg_inv[d], -0.5f);
+    int c = __float_as_int(fminf(fmaxf(t, -1.0f), 4194304.0f) + 12582912.0f) - 0x4B400000;
     c = c < 0 ? 0 : c;
     return c >= P.bg_n[d] ? P.bg_n[d] - 1 : c;
 }
