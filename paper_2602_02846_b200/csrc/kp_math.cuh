@@ -247,11 +247,7 @@ KP_DEV Env env_view(const KpProblem& P, const float4* base) {
 
 KP_DEV int bg_cell(const KpProblem& P, float v, int d) {
     if (P.bg_n[d] == 1) return 0;  // uniform branch: undivided dimension
-    // floor(t) as rint(t - 0.5) with the magic add (no XU conversion): exact except at
-    // t == integer, where it may return the lower neighbour; obstacles touching a cell
-    // boundary are binned into both cells (margin), so the broad phase stays exact
-    const float t = fmaf(v - P.bg_lo[d], P.bg_inv[d], -0.5f);
-    int c = __float_as_int(fminf(fmaxf(t, -1.0f), 4194304.0f) + 12582912.0f) - 0x4B400000;
+    int c = __float2int_rd((v - P.bg_lo[d]) * P.bg_inv[d]);
     c = c < 0 ? 0 : c;
     return c >= P.bg_n[d] ? P.bg_n[d] - 1 : c;
 }
