@@ -289,6 +289,10 @@ def run_b200(args, scenario):
                "first_solution_cost": r["best_cost"] if r["found"] else None,
                "iterations": r["iterations"]}
 
+    extras = {}
+    if rank == 0 and ws == 1 and not args.no_extras:
+        extras = other_configs(args, budget)
+
     if rank == 0:
         ttfs = [r["first_solution_s"] * 1e3 for r in results if r["found"]]
         costs = [r["best_cost"] for r in results if r["found"]]
@@ -324,12 +328,76 @@ def run_b200(args, scenario):
                     "note": "host wall clock around kp_reset_query + kp_solve + kp_get_path per query"},
             "clocks": clk.summary(),
             "gpu_launches": launches,
+            "other_configs": extras,
         }
         print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
     planner.close()
     return 0
+
+
+def other_configs(args, budget):
+    """The other BASELINE configs, summarised in the headline line (each guarded):
+    Dubins6/narrow and Quad12/building single queries (config 2, 3), a batch
+    through the concurrent engine (config 4) and the Quad12 propagate sweep's
+    saturated roofline (config 5)."""
+    from paper_2602_02846_b200 import BatchPlanner, Planner, scenarios
+
+    out = {}
+    for cfg in ("narrow_dubins6", "building_quad12"):
+        try:
+            s = scenarios.load(cfg)
+            b = budget if cfg != "building_quad12" else max(budget, 0.1)
+            with Planner(s, seed=args.seed_base) as g:
+                g.reset(1)
+                g.solve(b)
+                res, dev = [], 0.0
+                for i in range(5):
+                    g.reset(args.seed_base + i)
+                    r = g.solve(b)
+                    res.append(r)
+                    dev += r["elapsed_s"]
+            tt = [r["first_solution_s"] * 1e3 for r in res if r["found"]]
+            out[cfg] = {"budget_ms": b * 1e3, "queries": len(res), "success_rate": len(tt) / len(res),
+                        "ms_to_first_solution_median": _median(tt),
+                        "solution_cost_at_budget_median": _median([r["best_cost"] for r in res if r["found"]]),
+                        "node_propagations_per_sec": sum(r["propagations_attempted"] for r in res) / dev}
+        except Exception as e:  # noqa: BLE001
+            out[cfg] = {"error": str(e)[:200]}
+    try:
+        s = scenarios.load(args.config, capacity=1 << 19, max_slots=1 << 21)
+        with BatchPlanner(s, lanes=8) as bp:
+            bp.solve(range(900000, 900008), budget)
+            res, wall = bp.solve(range(args.seed_base, args.seed_base + 64), budget)
+        tt = [r["first_solution_s"] * 1e3 for r in res if r["found"]]
+        out["batch_" + args.config] = {
+            "queries": len(res), "lanes": 8, "budget_ms": budget * 1e3, "wall_s": wall,
+            "queries_per_s": len(res) / wall,
+            "node_propagations_per_sec": sum(r["propagations_attempted"] for r in res) / wall,
+            "ms_to_first_solution_median": _median(tt), "success_rate": len(tt) / len(res)}
+    except Exception as e:  # noqa: BLE001
+        out["batch_" + args.config] = {"error": str(e)[:200]}
+    try:
+        s = scenarios.load("building_quad12")
+        s["planner"]["capacity"] = max(int(s["planner"]["capacity"]), (1 << 22) // 32)
+        s["planner"]["max_slots"] = 1 << 22
+        pk = _peaks()
+        with Planner(s, seed=1) as g:
+            g.sweep(1 << 10, launches=2)
+            rows = []
+            for k in (18, 20, 22):
+                ms, one = g.sweep((1 << k) // 32, launches=3)
+                ops = (one["rk4_steps"] * OPS_PER_STEP["quadcopter_12d"] + one["items"] * OPS_PER_ITEM
+                       + one["box_tests"] * OPS_PER_BOX + one["sphere_tests"] * OPS_PER_SPHERE
+                       + one["interp_points"] * OPS_PER_INTERP)
+                rows.append({"k": k, "items_per_s": one["items"] / (ms * 1e-3),
+                             "frac": ops / (ms * 1e-3) / pk["fp32_lane_ops"]})
+        out["sweep_building_quad12"] = {"kernel": "k_propagate<3>", "bound": "fp32", "peak_src": pk["fp32_src"],
+                                        "rows": rows, "best_frac": max(r["frac"] for r in rows)}
+    except Exception as e:  # noqa: BLE001
+        out["sweep_building_quad12"] = {"error": str(e)[:200]}
+    return out
 
 
 def _quart(xs):
@@ -503,6 +571,7 @@ def main():
     ap.add_argument("--seed-base", type=int, default=1000)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the other-config summaries")
     ap.add_argument("--sweep", action="store_true", help="BASELINE config 5: propagate throughput sweep")
     ap.add_argument("--batch", type=int, default=0, help="BASELINE config 4: number of queries in the batch")
     ap.add_argument("--lanes", type=int, default=16, help="concurrent planner lanes per GPU (--batch)")
