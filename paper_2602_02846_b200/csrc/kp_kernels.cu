@@ -52,10 +52,10 @@ KP_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 KP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Stage the environment blob into shared memory (16-byte vector copies).
-KP_DEV Env stage_env(const KpProblem& P, const KpBuffers& B, float4* smem) {
-    for (uint32_t i = threadIdx.x; i < P.env_bytes / 16; i += blockDim.x) smem[i] = B.env[i];
+KP_DEV Env stage_env(const KpProblem& P, const KpBuffers& B) {
+    for (uint32_t i = threadIdx.x; i < P.env_bytes / 16; i += blockDim.x) kp_env_smem[i] = B.env[i];
     __syncthreads();
-    return env_view(P, smem);
+    return env_view(P);
 }
 
 // Propagate (Alg. 2).  Work is claimed by blocks in chunks of 256*G slots
@@ -83,17 +83,12 @@ struct PropSmem {
 };
 
 template <int MODEL>
-__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propagate(KpProblem P, KpBuffers B) {
+KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MODEL>& sh, const Env& E) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
-    extern __shared__ float4 smem4[];
-    __shared__ PropSmem<MODEL> sh;
     KpCtl* ctl = B.ctl;
-    if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
-    const Env E = stage_env(P, B, smem4);  // constant data: overlaps the predecessor's tail
-    pdl_wait();
-    pdl_trigger();
     if (ctl->done) return;
+    if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
     const uint32_t n_items = ctl->n_items;
     const uint32_t G = min(KP_PROP_MAXG, max(1u, n_items / (KP_PROP_THREADS * gridDim.x)));
@@ -102,7 +97,7 @@ __global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propa
     if (blockIdx.x >= n_chunks) return;  // nothing for this block this iteration
     const uint32_t it = ctl->iter;
     const unsigned long long seed = ctl->seed;
-    const uint32_t* __restrict__ va = B.va[it & 1];
+    const uint32_t* va = B.va[it & 1];  // (no __restrict__: rewritten across iterations in persistent mode)
     const uint32_t cap = P.capacity, S_cap = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -226,6 +221,15 @@ __global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propa
     }
 }
 
+template <int MODEL>
+__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propagate(KpProblem P, KpBuffers B) {
+    __shared__ PropSmem<MODEL> sh;
+    const Env E = stage_env(P, B);  // constant data: overlaps the predecessor's tail
+    pdl_wait();
+    pdl_trigger();
+    propagate_phase<MODEL>(P, B, sh, E);
+}
+
 // Block-wide inclusive sum of three counters (blockDim == KP_SELECT_THREADS).
 struct Cnt3 {
     uint32_t k, v, c;
@@ -314,10 +318,8 @@ KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, ui
     return KP_ST_ACTIVE;
 }
 
-__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P, KpBuffers B) {
+KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
     KpCtl* ctl = B.ctl;
-    pdl_wait();
-    pdl_trigger();
     if (ctl->done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_sel_ns = globaltimer();
     __shared__ uint32_t s_st[7];
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
     const uint32_t n_tiles = (E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
     const uint32_t n_part = min(gridDim.x, n_tiles);  // participating blocks
     if (blockIdx.x >= n_part) return;
-    const uint32_t* __restrict__ live = B.live[it & 1];
+    const uint32_t* live = B.live[it & 1];
     uint32_t term = 0, deact = 0, react = 0, hops = 0, nlive = 0, nslot = 0, nadm = 0;
     if (threadIdx.x < 7) s_st[threadIdx.x] = 0;
     __syncthreads();
@@ -382,6 +384,12 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P
         if (s_st[5]) atomicAdd(&ctl->stats.slots_scanned, static_cast<unsigned long long>(s_st[5]));
         if (s_st[6]) atomicAdd(&ctl->stats.admitted_checked, static_cast<unsigned long long>(s_st[6]));
     }
+}
+
+__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P, KpBuffers B) {
+    pdl_wait();
+    pdl_trigger();
+    select_reduce_phase(P, B);
 }
 
 // Close an iteration: counts, stats, best / timeline / TTFS
@@ -466,10 +474,8 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
     }
 }
 
-__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem P, KpBuffers B) {
+KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     KpCtl* ctl = B.ctl;
-    pdl_wait();
-    pdl_trigger();
     if (ctl->done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_scat_ns = globaltimer();
     __shared__ unsigned int s_last;
@@ -528,10 +534,10 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     Cnt3 run{acc[0], acc[1], acc[2]};
     const uint32_t cap = P.capacity, S = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
-    const uint32_t* __restrict__ live = B.live[it & 1];
-    const uint32_t* __restrict__ va = B.va[it & 1];
-    uint32_t* __restrict__ live_n = B.live[(it + 1) & 1];
-    uint32_t* __restrict__ va_n = B.va[(it + 1) & 1];
+    const uint32_t* live = B.live[it & 1];
+    const uint32_t* va = B.va[it & 1];
+    uint32_t* live_n = B.live[(it + 1) & 1];
+    uint32_t* va_n = B.va[(it + 1) & 1];
     for (uint32_t tile = tb; tile < te; ++tile) {
         const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
         Cnt3 x{0, 0, 0};
@@ -597,6 +603,73 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     iteration_boundary(P, B, it, n_items, tot_keep, tot_va, tot_commit, n_nodes, accepted);
 }
 
+__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem P, KpBuffers B) {
+    pdl_wait();
+    pdl_trigger();
+    scatter_phase(P, B);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent mode: ONE cooperative launch runs every iteration of a solve.
+// The environment is staged once; the three phases are separated by a grid
+// barrier (sense reversal on a generation counter; every thread fences before
+// arriving, and the gpu-scope fence also invalidates the SM's L1, so data of
+// the previous phase is re-read from L2).  Spins are bounded by a watchdog
+// (ctl->error = 9) so a fault cannot hang the GPU.  Co-residency of all blocks
+// is guaranteed by cudaLaunchCooperativeKernel.
+#define KP_BARRIER_WATCHDOG_NS 2000000000ull
+
+KP_DEV bool grid_barrier(KpCtl* ctl) {
+    __threadfence();
+    __syncthreads();
+    __shared__ uint32_t s_ok;
+    if (threadIdx.x == 0) {
+        volatile uint32_t* gen = &ctl->bar_gen;
+        const uint32_t g = *gen;
+        uint32_t ok = 1;
+        if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
+            atomicExch(&ctl->bar_count, 0u);
+            __threadfence();
+            atomicAdd(&ctl->bar_gen, 1u);
+        } else {
+            const unsigned long long t0 = globaltimer();
+            while (*gen == g) {
+                if (globaltimer() - t0 > KP_BARRIER_WATCHDOG_NS) {
+                    ctl->error = 9;
+                    ok = 0;
+                    break;
+                }
+            }
+        }
+        __threadfence();
+        s_ok = ok;
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
+template <int MODEL>
+__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_persistent(KpProblem P, KpBuffers B) {
+    __shared__ PropSmem<MODEL> sh;
+    const Env E = stage_env(P, B);  // once per solve
+    KpCtl* ctl = B.ctl;
+    for (;;) {
+        __shared__ uint32_t s_stop;
+        if (threadIdx.x == 0) {
+            const volatile KpCtl* vc = ctl;
+            s_stop = vc->done | vc->error;
+        }
+        __syncthreads();
+        if (s_stop) break;  // uniform across the grid: read after a barrier
+        propagate_phase<MODEL>(P, B, sh, E);
+        if (!grid_barrier(ctl)) break;
+        select_reduce_phase(P, B);
+        if (!grid_barrier(ctl)) break;
+        scatter_phase(P, B);  // its last block closes the iteration
+        if (!grid_barrier(ctl)) break;
+    }
+}
+
 // Reset the region table and plant the root (Alg. 1 lines 1-5).
 __global__ void k_reset_table(KpProblem P, KpBuffers B) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_regions; i += gridDim.x * blockDim.x)
@@ -658,8 +731,7 @@ __global__ void k_debug_propagate(KpProblem P, KpBuffers B, uint32_t n, const fl
                                   uint8_t* goals) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
-    extern __shared__ float4 smem4[];
-    const Env E = stage_env(P, B, smem4);
+    const Env E = stage_env(P, B);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float x[N], u[M], dt;
@@ -792,6 +864,31 @@ cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_pr
     return e;
 }
 
+int persistent_occupancy(const KpProblem& P) {
+    int nb = 0;
+    const size_t smem = propagate_smem(P);
+    switch (P.model) {
+        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<0>, KP_PROP_THREADS, smem); break;
+        case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<1>, KP_PROP_THREADS, smem); break;
+        case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<2>, KP_PROP_THREADS, smem); break;
+        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<3>, KP_PROP_THREADS, smem); break;
+    }
+    return nb;
+}
+
+cudaError_t launch_persistent(const KpProblem& P, const KpBuffers& B, int grid, cudaStream_t st) {
+    void* args[] = {const_cast<KpProblem*>(&P), const_cast<KpBuffers*>(&B)};
+    const size_t smem = propagate_smem(P);
+    const void* fn = nullptr;
+    switch (P.model) {
+        case 0: fn = reinterpret_cast<const void*>(k_persistent<0>); break;
+        case 1: fn = reinterpret_cast<const void*>(k_persistent<1>); break;
+        case 2: fn = reinterpret_cast<const void*>(k_persistent<2>); break;
+        default: fn = reinterpret_cast<const void*>(k_persistent<3>); break;
+    }
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(KP_PROP_THREADS), args, smem, st);
+}
+
 cudaError_t set_propagate_smem(const KpProblem& P) {
     const int smem = static_cast<int>(propagate_smem(P));
     cudaError_t e = cudaSuccess;
@@ -800,6 +897,13 @@ cudaError_t set_propagate_smem(const KpProblem& P) {
         case 1: e = cudaFuncSetAttribute(k_propagate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
         case 2: e = cudaFuncSetAttribute(k_propagate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
         default: e = cudaFuncSetAttribute(k_propagate<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+    }
+    if (e != cudaSuccess) return e;
+    switch (P.model) {
+        case 0: e = cudaFuncSetAttribute(k_persistent<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 1: e = cudaFuncSetAttribute(k_persistent<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 2: e = cudaFuncSetAttribute(k_persistent<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        default: e = cudaFuncSetAttribute(k_persistent<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
     }
     return e;
 }

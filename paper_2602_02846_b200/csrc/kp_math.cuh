@@ -226,23 +226,45 @@ KP_DEV int step_count(const KpProblem& P, float dt) {
 }
 
 // --------------------------------------------------------- environment ----
-// Environment view over the shared-memory copy of the blob (kp_types.h).
-struct Env {
-    const float4* blo;
-    const float4* bhi;
-    const float4* sph;
-    const uint32_t* cells;
-    const uint16_t* cids;
+// The environment blob (kp_types.h) lives in dynamic shared memory.  It is
+// addressed through this extern __shared__ array (never through generic
+// pointers), so every access compiles to a plain LDS with no per-access
+// shared-window conversion.
+extern __shared__ float4 kp_env_smem[];
+
+struct Env {  // 32-bit shared-window base of kp_env_smem + byte offsets inside it
+    uint32_t base, off_bhi, off_sph, off_cells, off_cids;
 };
 
-KP_DEV Env env_view(const KpProblem& P, const float4* base) {
+KP_DEV uint32_t env_saddr();
+
+KP_DEV Env env_view(const KpProblem& P) {
     Env e;
-    e.blo = base;
-    e.bhi = base + P.n_box;
-    e.sph = base + 2 * P.n_box;
-    e.cells = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(base) + P.off_cells);
-    e.cids = reinterpret_cast<const uint16_t*>(reinterpret_cast<const char*>(base) + P.off_cids);
+    e.base = env_saddr();  // once per kernel: the window conversion reads a special register
+    e.off_bhi = 16u * static_cast<uint32_t>(P.n_box);
+    e.off_sph = 32u * static_cast<uint32_t>(P.n_box);
+    e.off_cells = P.off_cells;
+    e.off_cids = P.off_cids;
     return e;
+}
+
+// 32-bit shared-window address of the blob and typed ld.shared helpers
+// (non-volatile: the compiler may still schedule / batch them).
+KP_DEV uint32_t env_saddr() { return static_cast<uint32_t>(__cvta_generic_to_shared(kp_env_smem)); }
+KP_DEV uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+KP_DEV uint32_t lds_u16(uint32_t a) {
+    unsigned short v;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+KP_DEV float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
 }
 
 KP_DEV int bg_cell(const KpProblem& P, float v, int d) {
@@ -259,17 +281,19 @@ KP_DEV int bg_cell(const KpProblem& P, float v, int d) {
 KP_DEV bool in_obstacle(const KpProblem& P, const Env& E, float px, float py, float pz, uint32_t& nbox,
                         uint32_t& nsph) {
     const int c = bg_cell(P, px, 0) + P.bg_n[0] * (bg_cell(P, py, 1) + P.bg_n[1] * bg_cell(P, pz, 2));
-    const uint32_t range = E.cells[c];
+    const uint32_t base = E.base;
+    const uint32_t range = lds_u32(base + E.off_cells + 4u * static_cast<uint32_t>(c));
     const int b = static_cast<int>(range & 0xFFFFu), e = static_cast<int>(range >> 16);
     for (int k = b; k < e; ++k) {
-        const int id = E.cids[k];
+        const int id = static_cast<int>(lds_u16(base + E.off_cids + 2u * static_cast<uint32_t>(k)));
         if (id < P.n_box) {
-            const float4 lo = E.blo[id], hi = E.bhi[id];
+            const float4 lo = lds_f4(base + 16u * static_cast<uint32_t>(id));
+            const float4 hi = lds_f4(base + E.off_bhi + 16u * static_cast<uint32_t>(id));
             ++nbox;
             const bool in = (px >= lo.x) & (px <= hi.x) & (py >= lo.y) & (py <= hi.y) & (pz >= lo.z) & (pz <= hi.z);
             if (in) return true;
         } else {
-            const float4 o = E.sph[id - P.n_box];
+            const float4 o = lds_f4(base + E.off_sph + 16u * static_cast<uint32_t>(id - P.n_box));
             ++nsph;
             const float dx = px - o.x, dy = py - o.y, dz = pz - o.z;
             float d2 = dx * dx;
