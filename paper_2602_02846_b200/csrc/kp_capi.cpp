@@ -33,8 +33,7 @@ namespace kp {
 cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_prop, int grid_sel, cudaStream_t st,
                              int which);
 cudaError_t set_propagate_smem(const KpProblem& P);
-int persistent_occupancy(const KpProblem& P);
-cudaError_t launch_persistent(const KpProblem& P, const KpBuffers& B, int grid, cudaStream_t st);
+
 int propagate_occupancy(const KpProblem& P);
 cudaError_t launch_reset(const KpProblem& P, const KpBuffers& B, unsigned long long seed, cudaStream_t st);
 cudaError_t launch_start(const KpBuffers& B, unsigned long long budget_ns, uint32_t max_iters, uint32_t stop_first,
@@ -67,14 +66,6 @@ void cuda_check(cudaError_t e, const char* what) {
 
 thread_local std::string g_create_error;
 
-bool use_persistent() {
-    static const bool on = [] {
-        const char* e = std::getenv("KP_PERSISTENT");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 }  // namespace
 
 struct kp_planner {
@@ -83,7 +74,7 @@ struct kp_planner {
     kp_config_desc cfg{};
     int device = 0;
     int sms = 148;
-    int grid_prop = 0, grid_sel = 0, grid_persist = 0;
+    int grid_prop = 0, grid_sel = 0;
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph = nullptr;
     uint32_t* host_done = nullptr;  // pinned, mapped
@@ -632,11 +623,7 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         const int occ = std::max(1, kp::propagate_occupancy(P));
         pl->grid_prop = pl->sms * occ;
         pl->grid_sel = pl->sms * 4;
-        int pocc = 0;
-        int coop = 0;
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
-        if (coop) pocc = kp::persistent_occupancy(P);
-        pl->grid_persist = pocc > 0 ? pl->sms * pocc : 0;
+
         for (auto*& e : pl->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
         do_reset(pl, config->seed);
         capture_graph(pl);
@@ -777,17 +764,6 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
                 }
                 if (wall() > watchdog) throw KpError(KP_ERR_CUDA, "solve watchdog expired (device did not finish)");
             }
-        } else if (use_persistent() && pl->grid_persist > 0) {
-            // one cooperative launch runs every iteration (grid barriers between phases)
-            cuda_check(kp::launch_persistent(pl->P, pl->B, pl->grid_persist, pl->stream), "persistent launch");
-            pl->kernel_launches += 1;
-            for (;;) {
-                if (*done) break;
-                const cudaError_t q = cudaStreamQuery(pl->stream);
-                if (q == cudaSuccess) break;
-                if (q != cudaErrorNotReady) cuda_check(q, "persistent kernel");
-                if (wall() > watchdog) throw KpError(KP_ERR_CUDA, "solve watchdog expired (persistent kernel)");
-            }
         } else {
             // keep at most two graphs in flight; stop as soon as the device
             // raises the mapped done word
@@ -813,7 +789,6 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
             }
         }
         fetch_ctl(pl);
-        if (pl->ctl.error == 9) throw KpError(KP_ERR_CUDA, "device watchdog: a grid barrier did not complete");
         if (pl->ctl.error == 8)
             throw KpError(KP_ERR_SLOT_OVERFLOW, "lambda*|V_A| exceeded max_slots; raise kp_config_desc.max_slots");
         fill_result(pl, out);

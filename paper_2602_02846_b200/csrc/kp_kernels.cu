@@ -609,67 +609,6 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem 
     scatter_phase(P, B);
 }
 
-// ---------------------------------------------------------------------------
-// Persistent mode: ONE cooperative launch runs every iteration of a solve.
-// The environment is staged once; the three phases are separated by a grid
-// barrier (sense reversal on a generation counter; every thread fences before
-// arriving, and the gpu-scope fence also invalidates the SM's L1, so data of
-// the previous phase is re-read from L2).  Spins are bounded by a watchdog
-// (ctl->error = 9) so a fault cannot hang the GPU.  Co-residency of all blocks
-// is guaranteed by cudaLaunchCooperativeKernel.
-#define KP_BARRIER_WATCHDOG_NS 2000000000ull
-
-KP_DEV bool grid_barrier(KpCtl* ctl) {
-    __threadfence();
-    __syncthreads();
-    __shared__ uint32_t s_ok;
-    if (threadIdx.x == 0) {
-        volatile uint32_t* gen = &ctl->bar_gen;
-        const uint32_t g = *gen;
-        uint32_t ok = 1;
-        if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
-            atomicExch(&ctl->bar_count, 0u);
-            __threadfence();
-            atomicAdd(&ctl->bar_gen, 1u);
-        } else {
-            const unsigned long long t0 = globaltimer();
-            while (*gen == g) {
-                if (globaltimer() - t0 > KP_BARRIER_WATCHDOG_NS) {
-                    ctl->error = 9;
-                    ok = 0;
-                    break;
-                }
-            }
-        }
-        __threadfence();
-        s_ok = ok;
-    }
-    __syncthreads();
-    return s_ok != 0;
-}
-
-template <int MODEL>
-__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_persistent(KpProblem P, KpBuffers B) {
-    __shared__ PropSmem<MODEL> sh;
-    const Env E = stage_env(P, B);  // once per solve
-    KpCtl* ctl = B.ctl;
-    for (;;) {
-        __shared__ uint32_t s_stop;
-        if (threadIdx.x == 0) {
-            const volatile KpCtl* vc = ctl;
-            s_stop = vc->done | vc->error;
-        }
-        __syncthreads();
-        if (s_stop) break;  // uniform across the grid: read after a barrier
-        propagate_phase<MODEL>(P, B, sh, E);
-        if (!grid_barrier(ctl)) break;
-        select_reduce_phase(P, B);
-        if (!grid_barrier(ctl)) break;
-        scatter_phase(P, B);  // its last block closes the iteration
-        if (!grid_barrier(ctl)) break;
-    }
-}
-
 // Reset the region table and plant the root (Alg. 1 lines 1-5).
 __global__ void k_reset_table(KpProblem P, KpBuffers B) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_regions; i += gridDim.x * blockDim.x)
@@ -864,31 +803,6 @@ cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_pr
     return e;
 }
 
-int persistent_occupancy(const KpProblem& P) {
-    int nb = 0;
-    const size_t smem = propagate_smem(P);
-    switch (P.model) {
-        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<0>, KP_PROP_THREADS, smem); break;
-        case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<1>, KP_PROP_THREADS, smem); break;
-        case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<2>, KP_PROP_THREADS, smem); break;
-        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<3>, KP_PROP_THREADS, smem); break;
-    }
-    return nb;
-}
-
-cudaError_t launch_persistent(const KpProblem& P, const KpBuffers& B, int grid, cudaStream_t st) {
-    void* args[] = {const_cast<KpProblem*>(&P), const_cast<KpBuffers*>(&B)};
-    const size_t smem = propagate_smem(P);
-    const void* fn = nullptr;
-    switch (P.model) {
-        case 0: fn = reinterpret_cast<const void*>(k_persistent<0>); break;
-        case 1: fn = reinterpret_cast<const void*>(k_persistent<1>); break;
-        case 2: fn = reinterpret_cast<const void*>(k_persistent<2>); break;
-        default: fn = reinterpret_cast<const void*>(k_persistent<3>); break;
-    }
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(KP_PROP_THREADS), args, smem, st);
-}
-
 cudaError_t set_propagate_smem(const KpProblem& P) {
     const int smem = static_cast<int>(propagate_smem(P));
     cudaError_t e = cudaSuccess;
@@ -898,13 +812,7 @@ cudaError_t set_propagate_smem(const KpProblem& P) {
         case 2: e = cudaFuncSetAttribute(k_propagate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
         default: e = cudaFuncSetAttribute(k_propagate<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
     }
-    if (e != cudaSuccess) return e;
-    switch (P.model) {
-        case 0: e = cudaFuncSetAttribute(k_persistent<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-        case 1: e = cudaFuncSetAttribute(k_persistent<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-        case 2: e = cudaFuncSetAttribute(k_persistent<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-        default: e = cudaFuncSetAttribute(k_persistent<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-    }
+
     return e;
 }
 

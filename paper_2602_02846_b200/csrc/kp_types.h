@@ -103,7 +103,6 @@ struct KpCtl {
     uint32_t tot_keep, tot_va, tot_commit, accepted;
     uint32_t ticket_a, ticket_b;
     uint32_t prop_cursor;     // dynamic chunk cursor of k_propagate (reset at every boundary)
-    uint32_t bar_count, bar_gen;  // grid barrier of the persistent kernel
     // run bookkeeping
     uint32_t max_iter_abs;    // stop when iter >= this (0 = unlimited)
     uint32_t stop_first;
