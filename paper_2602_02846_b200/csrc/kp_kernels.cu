@@ -97,7 +97,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     if (blockIdx.x >= n_chunks) return;  // nothing for this block this iteration
     const uint32_t it = ctl->iter;
     const unsigned long long seed = ctl->seed;
-    const uint32_t* va = B.va[it & 1];  // (no __restrict__: rewritten across iterations in persistent mode)
+    const uint32_t* va = B.va[it & 1];
     const uint32_t cap = P.capacity, S_cap = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -141,3 +141,48 @@ def test_solve_continues_and_reset_repeats():
         c = g.solve(budget_s=0.0, max_iterations=12)
         assert c["node_count"] == b["node_count"] and c["best_cost"] == b["best_cost"]
         assert a["iterations"] == 6
+
+
+def test_control_duration_cost_whole_run():
+    """CostKind::ControlDuration (cost.hpp:15, :50-51): segment cost = dt."""
+    s = scenarios.load("forest_di6")
+    s["problem"]["cost"] = "control_duration"
+    with Planner(s, seed=8) as g:
+        rg = g.solve(budget_s=0.0, max_iterations=12)
+        o = kpo.Oracle(s, kpo.MIRROR32, seed=8, workers=8)
+        ro = o.run(budget_s=0.0, max_iterations=12, stop_first=0)
+        _compare_runs(g, o, rg, ro)
+
+
+@pytest.mark.parametrize("obstacles", [[], [{"type": "sphere", "center": [5, 5, 5], "radius": 2.0},
+                                            {"type": "sphere", "center": [2, 8, 3], "radius": 1.0}]])
+def test_empty_and_sphere_environments(obstacles):
+    s = scenarios.load("forest_di6")
+    s["problem"]["environment"]["obstacles"] = obstacles
+    with Planner(s, seed=4) as g:
+        rg = g.solve(budget_s=0.0, max_iterations=10)
+        o = kpo.Oracle(s, kpo.MIRROR32, seed=4, workers=8)
+        ro = o.run(budget_s=0.0, max_iterations=10, stop_first=0)
+        _compare_runs(g, o, rg, ro)
+
+
+def test_new_start_state_query():
+    s = scenarios.load("forest_di6")
+    start = [5.2, 0.7, 2.0, 0.5, 0.0, -0.25]
+    with Planner(s) as g:
+        g.reset(6, x_init=start)
+        rg = g.solve(budget_s=0.0, max_iterations=10)
+        s2 = scenarios.load("forest_di6")
+        s2["problem"]["x_init"] = start
+        o = kpo.Oracle(s2, kpo.MIRROR32, seed=6, workers=8)
+        ro = o.run(budget_s=0.0, max_iterations=10, stop_first=0)
+        _compare_runs(g, o, rg, ro)
+
+
+def test_slot_overflow_fails_loudly():
+    from paper_2602_02846_b200.planner import KinoplanError
+
+    s = scenarios.load("forest_di6", max_slots=4096)
+    with Planner(s, seed=1) as g:
+        with pytest.raises(KinoplanError, match="max_slots"):
+            g.solve(budget_s=0.0, max_iterations=20)
