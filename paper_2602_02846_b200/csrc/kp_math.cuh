@@ -311,11 +311,18 @@ template <int MODEL>
 KP_DEV bool within_bounds(const KpProblem& P, const float* x) {
     constexpr int N = Model<MODEL>::N;
     // state bounds with the workspace bounds folded into the
-    // position dims on the host: x >= max(lo_s, lo_w) <=> x >= lo_s && x >= lo_w
-    bool ok = true;
+    // position dims on the host: x >= max(lo_s, lo_w) <=> x >= lo_s && x >= lo_w.
+    // Three independent compare chains (the predicate-accumulating FSETP form
+    // is serial) combined at the end: shorter dependent path per RK4 step.
+    bool ok0 = true, ok1 = true, ok2 = true;
 #pragma unroll
-    for (int i = 0; i < N; ++i) ok = ok & (x[i] >= P.blo[i]) & (x[i] <= P.bhi[i]);
-    return ok;
+    for (int i = 0; i < N; ++i) {
+        const bool in = (x[i] >= P.blo[i]) & (x[i] <= P.bhi[i]);
+        if (i % 3 == 0) ok0 = ok0 & in;
+        else if (i % 3 == 1) ok1 = ok1 & in;
+        else ok2 = ok2 & in;
+    }
+    return ok0 & ok1 & ok2;
 }
 
 // x[d] for a runtime d without spilling x to local memory (fully unrolled select).
@@ -398,8 +405,11 @@ KP_DEV int integrate_item(const KpProblem& P, const Env& E, float* x, const floa
         if (!rk4_step<MODEL>(P, x, u, hk, sixth)) return 2;
         o.steps += 1;
         const float nx = x[0], ny = x[1], nz = TWO_D ? 0.0f : x[2];
-        if (!within_bounds<MODEL>(P, x)) return 1;
-        if (in_obstacle(P, E, nx, ny, nz, o.nbox, o.nsph)) return 1;
+        // bounds and obstacle test without a branch in between (one exit per step;
+        // the broad-phase cell index is clamped, so out-of-bounds states are safe)
+        const bool inb = within_bounds<MODEL>(P, x);
+        const bool hit = in_obstacle(P, E, nx, ny, nz, o.nbox, o.nsph);
+        if (!inb || hit) return 1;
         const float dx = nx - px, dy = ny - py, dz = nz - pz;
         float d2 = dx * dx;
         d2 = fmaf(dy, dy, d2);
