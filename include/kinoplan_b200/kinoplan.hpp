@@ -183,6 +183,9 @@ struct PlannerStats {
     std::optional<std::pair<Scalar, Scalar>> first_solution;
     bool capacity_exhausted = false;
     Scalar elapsed = 0;
+    uint64_t first_solution_iteration = 0;  // iteration boundary that first set best < inf
+    uint64_t best_found_iteration = 0;
+    uint64_t node_count = 0;
 };
 
 struct Trajectory {

@@ -245,6 +245,9 @@ PlanResult Planner::solve(double budget_s, uint64_t max_iterations, bool extract
     s.nodes_committed = r.nodes_committed;
     s.capacity_exhausted = r.capacity_exhausted;
     s.elapsed = r.elapsed_s;
+    s.first_solution_iteration = r.first_solution_iteration;
+    s.best_found_iteration = r.best_found_iteration;
+    s.node_count = r.node_count;
     std::vector<kp_timeline_entry> tl(r.timeline_len);
     size_t len = 0;
     check(kp_get_timeline(h_, tl.data(), tl.size(), &len), h_);
