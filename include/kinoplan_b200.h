@@ -117,7 +117,7 @@ typedef struct kp_config_desc {
     int32_t deactivate_after_expansion; /* SPEC.md:436 ablation flag */
     int32_t rng_kind;           /* kp_rng_kind */
     int32_t stop_at_first_solution; /* stop at the first iteration boundary with best < inf */
-    uint64_t max_slots;         /* per-iteration V_U slot buffer; 0 = default */
+    uint64_t max_slots;         /* per-iteration V_U slot buffer; 0 = min(lambda*capacity, 2^25) */
 } kp_config_desc;
 
 /* BestSolution + PlannerStats. */

@@ -165,7 +165,7 @@ struct PlannerConfig {
     bool deactivate_after_expansion = false;
     RngKind rng = RngKind::Philox;
     bool stop_at_first_solution = false;
-    uint64_t max_slots = 0;         // per-iteration V_U slot buffer (0 = 2^22)
+    uint64_t max_slots = 0;         // per-iteration V_U slot buffer (0 = min(lambda*capacity, 2^25))
     int device = 0;
 };
 

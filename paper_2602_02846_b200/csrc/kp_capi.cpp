@@ -280,7 +280,10 @@ void build_problem(const kp_problem_desc* p, const kp_config_desc* c, KpProblem&
     P.rng_kind = c->rng_kind;
     P.deact = c->deactivate_after_expansion ? 1 : 0;
     P.capacity = static_cast<uint32_t>(c->capacity);
-    uint64_t slots = c->max_slots ? c->max_slots : (1ull << 22);
+    // Default: lambda * capacity (|V_A| <= live nodes <= capacity, so the
+    // buffer cannot overflow), capped at 2^25 slots (<= 2.7 GB for Quad12).
+    uint64_t slots = c->max_slots ? c->max_slots
+                                  : std::min<uint64_t>(static_cast<uint64_t>(c->lambda) * c->capacity, 1ull << 25);
     slots = (slots + 31) & ~31ull;
     if (slots > (1ull << 29)) throw KpError(KP_ERR_CONFIG, "max_slots too large (<= 2^29)");
     P.max_slots = static_cast<uint32_t>(slots);

@@ -12,7 +12,9 @@ the geometry of the BASELINE.json configs is pinned here:
   forest_di6       6D double integrator, trees (PAPER.md:687 env a)   27,000 regions
   narrow_dubins6   6D Dubins airplane, wall with one slot (env b)     52,000 regions
   building_quad12  12D quadcopter, rooms + doorways (env c)           100,000 regions
-plus the small 2-D scenes the SPEC examples use (free2d, zigzag2d).
+plus the SPEC's bundled set (free2d, zigzag2d, forest6d,
+narrow6d, building6d, zigzag6d, dubins_narrow, quad12d_forest, each also as
+`<name>_small`, the small-δ variant).
 """
 from __future__ import annotations
 
@@ -202,20 +204,136 @@ def zigzag2d() -> dict:
         },
         "decomposition": {"dims": [0, 1, 2, 3], "cells": [40, 40, 6, 6]},  # full state
         "planner": {
-            "lambda": 16, "i_max": 5, "t_prop": 0.8, "capacity": 1 << 18, "ode_step": 0.02,
+            "lambda": 16, "i_max": 5, "t_prop": 0.8, "capacity": 1 << 20, "ode_step": 0.02,
             "collision_step": 0.05, "t_max_ms": 100, "max_iterations": 0, "rng": "philox", "max_slots": 1 << 20,
         },
         "trials": {"n": 25, "base_seed": 0, "workers": 1},
     }
 
 
+# ---- the SPEC's bundled set: free2d, zigzag2d, forest6d,
+# narrow6d, building6d, zigzag6d, dubins_narrow, quad12d_forest, each with a
+# large-delta (as named) and a small-delta variant (`<name>_small`: every
+# decomposed position dimension split FINE times finer
+# "large-δ and small-δ variants").  forest6d / dubins_narrow are the BASELINE config 1 / 2
+# scenes under the SPEC's names.
+FINE = 2
+
+
+def _renamed(fn, name):
+    s = fn()
+    s["name"] = name
+    return s
+
+
+def _walls_narrow():
+    return copy.deepcopy(narrow_dubins6()["problem"]["environment"])
+
+
+def _di6(name, env, start, goal, cells, dims=(0, 1, 2), vmax=2.0, amax=2.0, t_max_ms=100, lam=32):
+    wb = env["workspace_bounds"]
+    return {
+        "name": name,
+        "problem": {
+            "model": "double_integrator_6d",
+            "model_params": {},
+            "environment": env,
+            "x_init": list(start) + [0.0, 0.0, 0.0],
+            "goal": {"dims": [0, 1, 2], "center": list(goal), "radius": 0.5},
+            "cost": "path_length",
+            "state_bounds": [list(b) for b in wb] + [[-vmax, vmax]] * 3,
+            "control_bounds": [[-amax, amax]] * 3,
+        },
+        "decomposition": {"dims": list(dims), "cells": list(cells)},
+        "planner": {
+            "lambda": lam, "i_max": 5, "t_prop": 0.5, "capacity": 1 << 20, "ode_step": 0.02,
+            "collision_step": 0.05, "t_max_ms": t_max_ms, "max_iterations": 0,
+            "deactivate_after_expansion": False, "rng": "philox",
+        },
+        "trials": {"n": 25, "base_seed": 0, "workers": 1},
+    }
+
+
+def narrow6d() -> dict:
+    """6D double integrator through the one-slot wall of narrow_dubins6."""
+    return _di6("narrow6d", _walls_narrow(), (1.0, 1.0, 2.5), (9.0, 9.0, 2.5), (30, 30, 15))
+
+
+def building6d() -> dict:
+    """6D double integrator in the four-room building of building_quad12."""
+    env = copy.deepcopy(building_quad12()["problem"]["environment"])
+    return _di6("building6d", env, (1.5, 1.5, 1.5), (8.5, 8.5, 1.5), (50, 50, 20))
+
+
+def zigzag6d() -> dict:
+    """6D double integrator through six staggered full-height walls (the 3-D
+    extrusion of zigzag2d); decomposition over position + planar velocity."""
+    obstacles = []
+    for i in range(6):
+        x0 = 1.2 + 1.4 * i
+        y0, y1 = (0.0, 7.0) if i % 2 == 0 else (3.0, 10.0)
+        obstacles.append({"type": "box", "min": [x0, y0, 0.0], "max": [x0 + 0.3, y1, 3.0]})
+    env = {"workspace_bounds": [[0, 10], [0, 10], [0, 3]], "obstacles": obstacles}
+    s = _di6("zigzag6d", env, (0.5, 0.5, 1.5), (9.5, 9.0, 1.5), (40, 40, 3, 4, 4), dims=(0, 1, 2, 3, 4),
+             vmax=1.5, amax=1.5)
+    s["planner"]["t_prop"] = 0.8
+    return s
+
+
+def quad12d_forest() -> dict:
+    """12D quadcopter among the forest_di6 trees (cut to the 4 m ceiling)."""
+    s = building_quad12()
+    trees = forest_di6()["problem"]["environment"]["obstacles"]
+    s["name"] = "quad12d_forest"
+    s["problem"]["environment"] = {
+        "workspace_bounds": [[0, 10], [0, 10], [0, 4]],
+        "obstacles": [{"type": "box", "min": t["min"], "max": [t["max"][0], t["max"][1], 4.0]} for t in trees],
+    }
+    s["problem"]["x_init"] = [0.5, 0.5, 2.0] + [0.0] * 9
+    s["problem"]["goal"]["center"] = [9.5, 9.5, 2.0]
+    s["decomposition"]["cells"] = [50, 50, 20]
+    s["planner"].pop("max_slots", None)
+    return s
+
+
+def small_delta(fn, fine: int = FINE):
+    """The small-δ variant of a scene: FINE× the cells on every decomposed
+    position dimension (velocity / angle cells unchanged)."""
+    def build():
+        s = fn()
+        s["name"] = s["name"] + "_small"
+        wdim = len(s["problem"]["environment"]["workspace_bounds"])
+        dec = s["decomposition"]
+        dec["cells"] = [c * fine if d < wdim else c for d, c in zip(dec["dims"], dec["cells"])]
+        # more regions keep more nodes alive: grow the store, size slots by default
+        s["planner"]["capacity"] = min(s["planner"]["capacity"] * 16, 1 << 23)
+        s["planner"].pop("max_slots", None)
+        return s
+    build.__name__ = fn.__name__ + "_small"
+    return build
+
+
+SPEC_SET = {
+    "free2d": free2d,
+    "zigzag2d": zigzag2d,
+    "forest6d": lambda: _renamed(forest_di6, "forest6d"),
+    "narrow6d": narrow6d,
+    "building6d": building6d,
+    "zigzag6d": zigzag6d,
+    "dubins_narrow": lambda: _renamed(narrow_dubins6, "dubins_narrow"),
+    "quad12d_forest": quad12d_forest,
+}
+
 BUILDERS = {
+    # BASELINE.json configs 1-3
     "forest_di6": forest_di6,
     "narrow_dubins6": narrow_dubins6,
     "building_quad12": building_quad12,
-    "free2d": free2d,
-    "zigzag2d": zigzag2d,
 }
+for _n, _f in SPEC_SET.items():
+    BUILDERS[_n] = _f
+    BUILDERS[_n + "_small"] = small_delta(_f)
+
 
 _REQUIRED = {
     "problem": ["model", "environment", "x_init", "goal", "state_bounds", "control_bounds"],
