@@ -291,6 +291,12 @@ void build_problem(const kp_problem_desc* p, const kp_config_desc* c, KpProblem&
     P.t_prop_d = c->t_prop;
     P.h = static_cast<float>(h);
     P.coll = static_cast<float>(c->collision_step);
+    {  // threshold on the squared distance: the interpolation test without the sqrt latency
+        float t = P.coll * P.coll;
+        while (std::sqrt(t) > P.coll) t = std::nextafter(t, 0.0f);
+        while (std::sqrt(std::nextafter(t, INFINITY)) <= P.coll) t = std::nextafter(t, INFINITY);
+        P.coll_d2 = t;
+    }
     P.zero_rate = static_cast<float>(1e-6);  // cost.hpp:30
     P.inv_m = 1.0f / static_cast<float>(mass);
     P.grav = static_cast<float>(gravity);
@@ -397,9 +403,12 @@ std::vector<uint8_t> build_env(KpProblem& P, const std::vector<float>& boxes, co
     }
     const int nc = n[0] * n[1] * n[2];
     for (int d = 0; d < 3; ++d) {
+        const bool divided = d < P.ws_dim && n[d] > 1;
         P.bg_n[d] = n[d];
+        P.bg_max[d] = n[d] - 1;
         P.bg_lo[d] = d < P.ws_dim ? static_cast<float>(lo[d]) : 0.0f;
-        P.bg_inv[d] = d < P.ws_dim ? static_cast<float>(1.0 / cell[d]) : 0.0f;
+        P.bg_inv[d] = divided ? static_cast<float>(1.0 / cell[d]) : 0.0f;
+        P.bg_off[d] = divided ? static_cast<float>(-lo[d] / cell[d]) : 0.0f;
     }
     std::vector<uint32_t> range(nc, 0);
     std::vector<uint16_t> ids;

@@ -240,7 +240,11 @@ KP_DEV uint32_t env_saddr();
 
 KP_DEV Env env_view(const KpProblem& P) {
     Env e;
-    e.base = env_saddr();  // once per kernel: the window conversion reads a special register
+    // once per kernel: the shared-window address of the blob involves a special
+    // register read (S2R SR_CgaCtaId); the volatile copy keeps the compiler
+    // from rematerialising that sequence at every use inside the step loop
+    const uint32_t a = env_saddr();
+    asm volatile("mov.b32 %0, %1;" : "=r"(e.base) : "r"(a));
     e.off_bhi = 16u * static_cast<uint32_t>(P.n_box);
     e.off_sph = 32u * static_cast<uint32_t>(P.n_box);
     e.off_cells = P.off_cells;
@@ -267,11 +271,13 @@ KP_DEV float4 lds_f4(uint32_t a) {
     return v;
 }
 
+// Broad-phase cell of v along d: floor(v * inv + off) clamped to [0, n-1].
+// Branch-free: an undivided dim has inv = off = 0 (cell 0; NaN converts to 0).
+// The binning need not be exact: the host lists every obstacle in all cells
+// its AABB touches with a margin of 1e-3 cell, far above this rounding.
 KP_DEV int bg_cell(const KpProblem& P, float v, int d) {
-    if (P.bg_n[d] == 1) return 0;  // uniform branch: undivided dimension
-    int c = __float2int_rd((v - P.bg_lo[d]) * P.bg_inv[d]);
-    c = c < 0 ? 0 : c;
-    return c >= P.bg_n[d] ? P.bg_n[d] - 1 : c;
+    const int c = __float2int_rd(fmaf(v, P.bg_inv[d], P.bg_off[d]));
+    return min(max(c, 0), P.bg_max[d]);
 }
 
 // Position inside some closed obstacle?  Broad phase: the
@@ -415,11 +421,17 @@ KP_DEV int integrate_item(const KpProblem& P, const Env& E, float* x, const floa
         d2 = fmaf(dy, dy, d2);
         if (!TWO_D) d2 = fmaf(dz, dz, d2);
         const float d = sqrtf(d2);
-        if (d > P.coll) {  // dyadic subdivision (nested points)
+        if (d2 > P.coll_d2) {  // == (d > P.coll); dyadic subdivision (nested points)
+            // k = 2^e: d / k and j / k are exact, so multiplying by the exact
+            // power-of-two reciprocal equals the division bit-for-bit
             int k = 2;
-            while (d / static_cast<float>(k) > P.coll && k < (1 << 24)) k <<= 1;
+            float rk = 0.5f;
+            while (d * rk > P.coll && k < (1 << 24)) {
+                k <<= 1;
+                rk *= 0.5f;
+            }
             for (int j = 1; j < k; ++j) {
-                const float t = static_cast<float>(j) / static_cast<float>(k);
+                const float t = static_cast<float>(j) * rk;
                 o.interp += 1;
                 if (in_obstacle(P, E, fmaf(t, dx, px), fmaf(t, dy, py), TWO_D ? 0.0f : fmaf(t, dz, pz), o.nbox,
                                 o.nsph))

@@ -48,6 +48,7 @@ struct KpProblem {
     uint32_t g_stride[KP_MAX_GRID];
     uint32_t n_regions;
     float t_prop, h, coll, zero_rate;
+    float coll_d2;           // sqrtf(x) > coll  <=>  x > coll_d2 (largest x with sqrtf(x) <= coll)
     double t_prop_d;
     float inv_m, grav, cx, cy, cz, inv_ix, inv_iy, inv_iz;
     int32_t lambda, i_max, rng_kind, deact;
@@ -60,8 +61,8 @@ struct KpProblem {
     // cell grid = exact broad phase: every obstacle whose (margin-expanded)
     // AABB overlaps a cell is listed in it, so the narrow-phase verdict equals
     // testing every obstacle ("outside every obstacle").
-    float bg_lo[3], bg_inv[3];
-    int32_t bg_n[3];
+    float bg_lo[3], bg_inv[3], bg_off[3];  // cell = floor(v * bg_inv + bg_off), bg_off = -bg_lo * bg_inv
+    int32_t bg_n[3], bg_max[3];
     int32_t n_cells, n_entries;
     uint32_t env_bytes;        // multiple of 16
     uint32_t off_cells, off_cids;  // byte offsets inside the blob
