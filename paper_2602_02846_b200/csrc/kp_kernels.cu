@@ -228,7 +228,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
 }
 
 template <int MODEL>
-__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 2 : 4)) k_propagate(KpProblem P, KpBuffers B) {
+__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 3 : 4)) k_propagate(KpProblem P, KpBuffers B) {
     __shared__ PropSmem<MODEL> sh;
     const Env E = stage_env(P, B);  // constant data: overlaps the predecessor's tail
     pdl_wait();
