@@ -219,7 +219,10 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     __syncthreads();
     if (threadIdx.x == 0) {
         if (sh.cnt[0]) atomicAdd(&ctl->stats.valid, sh.cnt[0]);
-        if (sh.cnt[1]) atomicAdd(&ctl->stats.admitted, sh.cnt[1]);
+        if (sh.cnt[1]) {
+            atomicAdd(&ctl->stats.admitted, sh.cnt[1]);
+            atomicAdd(&ctl->n_adm_iter, static_cast<uint32_t>(sh.cnt[1]));
+        }
         if (sh.cnt[2]) atomicAdd(&ctl->stats.rk4_steps, sh.cnt[2]);
         if (sh.cnt[3]) atomicAdd(&ctl->stats.interp_points, sh.cnt[3]);
         if (sh.cnt[4]) atomicAdd(&ctl->stats.box_tests, sh.cnt[4]);
@@ -324,49 +327,161 @@ KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, ui
     return KP_ST_ACTIVE;
 }
 
+// Slot elements are processed per 32-slot mask word (one thread per word):
+// the frontier is sparse in admitted / committed slots, so a word-level scan
+// touches 32x fewer elements than a slot-level one.  The set bits of a warp's
+// 32 words are then spread over the warp's lanes (one bit per lane per round,
+// bits in word order then bit order) so their memory round trips overlap.
+struct WarpBits {
+    uint32_t total;  // set bits over the warp's words (warp-uniform)
+    uint32_t excl;   // this lane's exclusive prefix
+};
+
+KP_DEV WarpBits warp_bits(uint32_t word) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t c = __popc(word);
+    uint32_t incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += y;
+    }
+    return {__shfl_sync(0xFFFFFFFFu, incl, 31), incl - c};
+}
+
+// Owner lane of the k-th set bit of the warp (smallest lane whose inclusive
+// prefix exceeds k).  Convergent: every lane must call it.
+KP_DEV int warp_bit_owner(const WarpBits& wb, uint32_t word, uint32_t k) {
+    const uint32_t incl = wb.excl + __popc(word);
+    int L = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, L + step - 1);
+        if (v <= k) L += step;
+    }
+    return L;
+}
+
+// Block-wide sums of three counters (blockDim == KP_SELECT_THREADS); the
+// result is valid in thread 0.  Ends with a barrier, so it can be reused.
+KP_DEV Cnt3 block_sum3(Cnt3 x) {
+    __shared__ uint32_t sr[3][KP_SELECT_THREADS / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        x.k += __shfl_down_sync(0xFFFFFFFFu, x.k, off);
+        x.v += __shfl_down_sync(0xFFFFFFFFu, x.v, off);
+        x.c += __shfl_down_sync(0xFFFFFFFFu, x.c, off);
+    }
+    if (lane == 0) { sr[0][warp] = x.k; sr[1][warp] = x.v; sr[2][warp] = x.c; }
+    __syncthreads();
+    Cnt3 t{0, 0, 0};
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int w = 0; w < KP_SELECT_THREADS / 32; ++w) { t.k += sr[0][w]; t.v += sr[1][w]; t.c += sr[2][w]; }
+    }
+    __syncthreads();
+    return t;
+}
+
+// Element layout of the two select kernels for this iteration (identical in
+// both): live nodes first, then the V_U slots either one per thread (dense:
+// many admitted slots, every commit test in its own thread) or one 32-slot
+// mask word per thread (sparse: 32x fewer elements to scan; the warp's set
+// bits are spread over its lanes).
+struct SelLayout {
+    bool sparse;
+    uint32_t slot0;   // first slot element (live part padded to a warp in the dense layout)
+    uint32_t E, n_tiles;
+};
+
+KP_DEV SelLayout sel_layout(uint32_t n_live, uint32_t n_items, uint32_t n_adm) {
+    SelLayout l;
+    const uint32_t n_words = (n_items + 31u) >> 5;
+    l.sparse = n_adm <= n_words;  // about one admitted slot per word or fewer: one round per warp
+    l.slot0 = l.sparse ? n_live : ((n_live + 31u) & ~31u);
+    l.E = l.slot0 + (l.sparse ? n_words : 32u * n_words);
+    l.n_tiles = (l.E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
+    return l;
+}
+
 KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
     KpCtl* ctl = B.ctl;
     if (ctl->done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_sel_ns = globaltimer();
     __shared__ uint32_t s_st[7];
+    __shared__ uint32_t s_cm[KP_SELECT_THREADS];  // commit words under construction (sparse layout)
     const uint32_t it = ctl->iter;
     const uint32_t n_live = ctl->n_live;
-    const uint32_t live_pad = (n_live + 31u) & ~31u;
     const uint32_t n_items = ctl->n_items;
-    const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
-    const uint32_t n_tiles = (E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
+    const SelLayout ly = sel_layout(n_live, n_items, ctl->n_adm_iter);
+    const uint32_t n_tiles = ly.n_tiles;
     const uint32_t n_part = min(gridDim.x, n_tiles);  // participating blocks
     if (blockIdx.x >= n_part) return;
     const uint32_t* live = B.live[it & 1];
+    const int lane = threadIdx.x & 31;
     uint32_t term = 0, deact = 0, react = 0, hops = 0, nlive = 0, nslot = 0, nadm = 0;
     if (threadIdx.x < 7) s_st[threadIdx.x] = 0;
     __syncthreads();
     for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
         Cnt3 x{0, 0, 0};
-        bool commit = false;
         if (e < n_live) {
             ++nlive;
             const uint8_t st = prune_node(P, B, live[e], &term, &deact, &react, &hops);
             x.k = st != KP_ST_TERMINAL;
             x.v = st == KP_ST_ACTIVE;
-        } else if (e >= live_pad && e < E) {
-            const uint32_t s = e - live_pad;
-            nslot += s < n_items;
-            if (s < n_items && ((B.admit_mask[s >> 5] >> (s & 31)) & 1u)) {
-                ++nadm;
-                commit = B.vu_acc[s] == B.rc[B.vu_region[s]];  // Alg. 4 line 3, bit-exact
-                x.c = commit;
+        }
+        const bool in_slots = e >= ly.slot0 && e < ly.E;
+        if (!ly.sparse) {  // one slot per thread; slot elements are warp-aligned
+            bool commit = false;
+            const uint32_t sl = e - ly.slot0;
+            if (in_slots) {
+                nslot += sl < n_items;
+                if (sl < n_items && ((B.admit_mask[sl >> 5] >> (sl & 31)) & 1u)) {
+                    ++nadm;
+                    commit = B.vu_acc[sl] == B.rc[B.vu_region[sl]];  // Alg. 4 line 3, bit-exact
+                    x.c = commit;
+                }
+            }
+            const uint32_t cm = __ballot_sync(0xFFFFFFFFu, commit);
+            if (in_slots && lane == 0) {
+                B.commit_mask[sl >> 5] = cm;
+                B.admit_mask[sl >> 5] = 0u;  // consumed: ready for the next propagate
+            }
+        } else {  // one mask word per thread
+            uint32_t w = 0, a = 0;
+            if (in_slots) {
+                w = e - ly.slot0;
+                a = B.admit_mask[w];
+                nslot += min(32u, n_items - 32u * w);
+            }
+            s_cm[threadIdx.x] = 0u;
+            const WarpBits wb = warp_bits(a);
+            __syncwarp();
+            for (uint32_t base = 0; base < wb.total; base += 32) {
+                const uint32_t k = base + lane;
+                const int L = warp_bit_owner(wb, a, k);
+                const uint32_t aL = __shfl_sync(0xFFFFFFFFu, a, L);
+                const uint32_t eL = __shfl_sync(0xFFFFFFFFu, wb.excl, L);
+                const uint32_t wL = __shfl_sync(0xFFFFFFFFu, w, L);
+                if (k < wb.total) {
+                    const uint32_t bit = __fns(aL, 0, static_cast<int>(k - eL) + 1);
+                    const uint32_t sl = 32u * wL + bit;
+                    ++nadm;
+                    if (B.vu_acc[sl] == B.rc[B.vu_region[sl]])  // Alg. 4 line 3, bit-exact
+                        atomicOr(&s_cm[(threadIdx.x & ~31u) + static_cast<uint32_t>(L)], 1u << bit);
+                }
+            }
+            __syncwarp();
+            if (in_slots) {
+                const uint32_t cm = s_cm[threadIdx.x];
+                x.c = __popc(cm);
+                B.commit_mask[w] = cm;
+                if (a) B.admit_mask[w] = 0u;  // consumed: ready for the next propagate
             }
         }
-        // slot elements are warp-aligned (live part padded to 32)
-        const uint32_t cm = __ballot_sync(0xFFFFFFFFu, commit);
-        if (e >= live_pad && e < E && (threadIdx.x & 31) == 0) {
-            B.commit_mask[(e - live_pad) >> 5] = cm;
-            B.admit_mask[(e - live_pad) >> 5] = 0u;  // consumed: ready for the next propagate
-        }
-        Cnt3 tot;
-        block_scan3(x, &tot);
+        const Cnt3 tot = block_sum3(x);
         if (threadIdx.x == 0) {
             B.tile_sums[tile] = tot.k;
             B.tile_sums[B.max_tiles + tile] = tot.v;
@@ -473,6 +588,7 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
     if (n_live1 == 0) done = true;
     ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
+    ctl->n_adm_iter = 0;
     if (done) {
         ctl->done = 1;
         __threadfence_system();
@@ -488,10 +604,9 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     __shared__ uint32_t s_red[6][KP_SELECT_THREADS / 32];
     const uint32_t it = ctl->iter;
     const uint32_t n_live = ctl->n_live;
-    const uint32_t live_pad = (n_live + 31u) & ~31u;
     const uint32_t n_items = ctl->n_items;
-    const uint32_t E = live_pad + ((n_items + 31u) & ~31u);
-    const uint32_t n_tiles = (E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
+    const SelLayout ly = sel_layout(n_live, n_items, ctl->n_adm_iter);  // as select_reduce
+    const uint32_t n_tiles = ly.n_tiles;
     const uint32_t n_part = min(gridDim.x, n_tiles);
     if (blockIdx.x >= n_part) return;
     // contiguous tile range of this block; exclusive prefix of its first tile
@@ -544,60 +659,86 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     const uint32_t* va = B.va[it & 1];
     uint32_t* live_n = B.live[(it + 1) & 1];
     uint32_t* va_n = B.va[(it + 1) & 1];
+    const int lane = threadIdx.x & 31;
+    // one committed slot -> node id n_nodes + rank (slot order), store, lists, best
+    auto commit_node = [&](uint32_t sl, uint32_t rank, bool goal) {
+        const uint32_t id = n_nodes + rank;
+#pragma unroll 4
+        for (int d = 0; d < P.n; ++d)
+            B.state[static_cast<size_t>(d) * cap + id] = B.vu_state[static_cast<size_t>(d) * S + sl];
+#pragma unroll 4
+        for (int d = 0; d < P.m; ++d)
+            B.ctrl[static_cast<size_t>(d) * cap + id] = B.vu_ctrl[static_cast<size_t>(d) * S + sl];
+        const uint32_t abits = B.vu_acc[sl];
+        B.dt[id] = B.vu_dt[sl];
+        B.acc[id] = abits;
+        const uint32_t par = va[sl / lam];
+        const uint32_t reg = B.vu_region[sl];
+        B.region[id] = reg;
+        B.parent[id] = static_cast<int32_t>(par);
+        B.link[id] = make_uint4(par, reg, abits, 0u);
+        B.status[id] = KP_ST_ACTIVE;
+        B.icnt[id] = 0;
+        live_n[tot_keep + rank] = id;
+        va_n[tot_va + rank] = id;
+        if (goal)  // Alg. 4 lines 5-7
+            atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
+    };
     for (uint32_t tile = tb; tile < te; ++tile) {
         const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
         Cnt3 x{0, 0, 0};
-        uint32_t g = 0, s = 0;
-        bool is_live = false, is_slot = false;
+        uint32_t g = 0, w = 0, cm = 0, gm = 0;
+        const bool in_slots = e >= ly.slot0 && e < ly.E;
         if (e < n_live) {
-            is_live = true;
             g = live[e];
             const uint8_t st = B.status[g];
             x.k = st != KP_ST_TERMINAL;
             x.v = st == KP_ST_ACTIVE;
-        } else if (e >= live_pad && e < E) {
-            s = e - live_pad;
-            if (s < n_items) {
-                is_slot = true;
-                x.c = (B.commit_mask[s >> 5] >> (s & 31)) & 1u;
+        } else if (in_slots) {
+            w = e - ly.slot0;  // slot (dense) or mask word (sparse)
+            if (!ly.sparse) {
+                if (w < n_items) {
+                    x.c = (B.commit_mask[w >> 5] >> (w & 31)) & 1u;
+                    gm = x.c ? (B.goal_mask[w >> 5] >> (w & 31)) & 1u : 0u;
+                }
+            } else {
+                cm = B.commit_mask[w];
+                gm = B.goal_mask[w];
+                x.c = __popc(cm);
             }
         }
-        const bool goal = is_slot && x.c && ((B.goal_mask[s >> 5] >> (s & 31)) & 1u);
         Cnt3 tot;
         const Cnt3 inc = block_scan3(x, &tot);  // (barrier: every lane has read its goal bit)
-        if (e >= live_pad && e < E && (threadIdx.x & 31) == 0) B.goal_mask[(e - live_pad) >> 5] = 0u;
         const uint32_t pk = run.k + inc.k - x.k;
         const uint32_t pv = run.v + inc.v - x.v;
-        const uint32_t pc = run.c + inc.c - x.c;
+        const uint32_t pc = run.c + inc.c - x.c;  // commits before this element (slot order)
         run.k += tot.k;
         run.v += tot.v;
         run.c += tot.c;
-        if (is_live && x.k) {
+        if (x.k) {
             live_n[pk] = g;
             if (x.v) va_n[pv] = g;
         }
-        if (is_slot && x.c && pc < accepted) {
-            const uint32_t id = n_nodes + pc;
-#pragma unroll 4
-            for (int d = 0; d < P.n; ++d)
-                B.state[static_cast<size_t>(d) * cap + id] = B.vu_state[static_cast<size_t>(d) * S + s];
-#pragma unroll 4
-            for (int d = 0; d < P.m; ++d)
-                B.ctrl[static_cast<size_t>(d) * cap + id] = B.vu_ctrl[static_cast<size_t>(d) * S + s];
-            const uint32_t abits = B.vu_acc[s];
-            B.dt[id] = B.vu_dt[s];
-            B.acc[id] = abits;
-            const uint32_t par = va[s / lam];
-            const uint32_t reg = B.vu_region[s];
-            B.region[id] = reg;
-            B.parent[id] = static_cast<int32_t>(par);
-            B.link[id] = make_uint4(par, reg, abits, 0u);
-            B.status[id] = KP_ST_ACTIVE;
-            B.icnt[id] = 0;
-            live_n[tot_keep + pc] = id;
-            va_n[tot_va + pc] = id;
-            if (goal)  // Alg. 4 lines 5-7
-                atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
+        if (!ly.sparse) {
+            if (in_slots && lane == 0) B.goal_mask[w >> 5] = 0u;  // consumed
+            if (x.c && pc < accepted) commit_node(w, pc, gm != 0u);
+        } else {
+            if (gm) B.goal_mask[w] = 0u;  // consumed
+            const WarpBits wb = warp_bits(cm);
+            for (uint32_t base = 0; base < wb.total; base += 32) {
+                const uint32_t k = base + lane;
+                const int L = warp_bit_owner(wb, cm, k);
+                const uint32_t cL = __shfl_sync(0xFFFFFFFFu, cm, L);
+                const uint32_t eL = __shfl_sync(0xFFFFFFFFu, wb.excl, L);
+                const uint32_t wL = __shfl_sync(0xFFFFFFFFu, w, L);
+                const uint32_t pL = __shfl_sync(0xFFFFFFFFu, pc, L);
+                const uint32_t gL = __shfl_sync(0xFFFFFFFFu, gm, L);
+                if (k >= wb.total) continue;
+                const uint32_t r = k - eL;
+                if (pL + r >= accepted) continue;  // store full
+                const uint32_t bit = __fns(cL, 0, static_cast<int>(r) + 1);
+                commit_node(32u * wL + bit, pL + r, ((gL >> bit) & 1u) != 0u);
+            }
         }
     }
     __threadfence();
@@ -661,6 +802,7 @@ __global__ void k_start(KpBuffers B, unsigned long long budget_ns, uint32_t max_
     ctl->ticket_a = 0;
     ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
+    ctl->n_adm_iter = 0;
     bool done = ctl->error != 0 || ctl->n_live == 0 || (stop_first && ctl->best != ~0ull);
     ctl->done = done ? 1u : 0u;
     __threadfence_system();
@@ -882,6 +1024,7 @@ __global__ void k_sweep_prepare(KpProblem P, KpBuffers B, uint32_t n) {
         c->n_va = n;
         c->n_items = n * static_cast<uint32_t>(P.lambda);
         c->prop_cursor = 0;
+        c->n_adm_iter = 0;
         c->stats = KpStats{};
     }
 }

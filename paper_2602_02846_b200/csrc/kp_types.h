@@ -104,6 +104,8 @@ struct KpCtl {
     uint32_t tot_keep, tot_va, tot_commit, accepted;
     uint32_t ticket_a, ticket_b;
     uint32_t prop_cursor;     // dynamic chunk cursor of k_propagate (reset at every boundary)
+    uint32_t n_adm_iter;      // slots admitted by this iteration's propagate (reset at every boundary);
+                              // selects the select kernels' element layout (per slot / per mask word)
     // run bookkeeping
     uint32_t max_iter_abs;    // stop when iter >= this (0 = unlimited)
     uint32_t stop_first;
