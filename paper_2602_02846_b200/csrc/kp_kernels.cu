@@ -429,6 +429,7 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
         if (e < n_live) {
             ++nlive;
             const uint8_t st = prune_node(P, B, live[e], &term, &deact, &react, &hops);
+            B.live_st[e] = st;  // scatter reads it by position, in parallel with live[e]
             x.k = st != KP_ST_TERMINAL;
             x.v = st == KP_ST_ACTIVE;
         }
@@ -691,7 +692,7 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         const bool in_slots = e >= ly.slot0 && e < ly.E;
         if (e < n_live) {
             g = live[e];
-            const uint8_t st = B.status[g];
+            const uint8_t st = B.live_st[e];
             x.k = st != KP_ST_TERMINAL;
             x.v = st == KP_ST_ACTIVE;
         } else if (in_slots) {
@@ -741,12 +742,17 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
             }
         }
     }
-    __threadfence();
+    // last block closes the iteration: the barrier orders the block's writes
+    // before thread 0's gpu-scope release (cumulative), the acquire of the
+    // last arriver makes every block's writes visible to it
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(&ctl->ticket_b, 1u) == n_part - 1);
+    if (threadIdx.x == 0) {
+        unsigned int prev;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctl->ticket_b) : "memory");
+        s_last = prev == n_part - 1;
+    }
     __syncthreads();
     if (!s_last || threadIdx.x != 0) return;
-    __threadfence();
     iteration_boundary(P, B, it, n_items, tot_keep, tot_va, tot_commit, n_nodes, accepted);
 }
 

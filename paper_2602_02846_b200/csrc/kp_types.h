@@ -130,6 +130,7 @@ struct KpBuffers {
     int32_t* parent;
     uint32_t* region;
     uint8_t* status;
+    uint8_t* live_st;    // [capacity] status after this iteration's prune, by live-list position
     uint16_t* icnt;
     // region table [n_regions], encoded fp32 bits (+inf = 0x7F800000)
     uint32_t* rc;
