@@ -439,8 +439,9 @@ def roofline(scenario, pa, pb):
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         cfg_name = scenario.get("name", "")
-        kname = f"kp::k_propagate<{ {'double_integrator_4d': 0, 'double_integrator_6d': 1, 'dubins_airplane_6d': 2, 'quadcopter_12d': 3}[model] }>"
-        traffic = tr.get(cfg_name, {}).get(kname, {}).get("dram_bytes")
+        mi = {'double_integrator_4d': 0, 'double_integrator_6d': 1, 'dubins_airplane_6d': 2, 'quadcopter_12d': 3}[model]
+        ent = tr.get(cfg_name, {})
+        traffic = (ent.get(f"k_propagate<{mi}>") or ent.get(f"kp::k_propagate<{mi}>") or {}).get("dram_bytes")
     except Exception:
         pass
     return {
