@@ -37,8 +37,14 @@ $(CLI): $(CSRC)/kinoplan_cli.cpp $(LIB) include/kinoplan_b200/bench.hpp
 oracle:
 	$(MAKE) -C oracle
 
+# Product library with the device invariant checks compiled in (KP_ASSERT in
+# kp_types.h): same path and name, so the GPU tests run against it unchanged.
+checks:
+	$(MAKE) -B $(LIB) NVFLAGS="$(NVFLAGS) -DKP_CHECKS"
+
+
 clean:
 	rm -f $(CSRC)/*.o $(LIB) $(CLI)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean checks

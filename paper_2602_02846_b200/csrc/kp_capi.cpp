@@ -30,6 +30,7 @@
 #include "kp_types.h"
 
 namespace kp {
+cudaError_t read_check_code(unsigned int* code);
 cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_prop, int grid_sel, cudaStream_t st,
                              int which);
 cudaError_t set_propagate_smem(const KpProblem& P);
@@ -464,10 +465,18 @@ void do_reset(kp_planner* pl, uint64_t seed) {
     cuda_check(cudaStreamSynchronize(pl->stream), "reset sync");
 }
 
+// Checks build (-DKP_CHECKS): raise on the first failed device invariant.
+void check_invariants() {
+    unsigned int code = 0;
+    cuda_check(kp::read_check_code(&code), "read check code");
+    if (code) throw KpError(KP_ERR_CUDA, "device invariant check " + std::to_string(code) + " failed");
+}
+
 void fetch_ctl(kp_planner* pl) {
     cuda_check(cudaMemcpyAsync(&pl->ctl, pl->B.ctl, sizeof(KpCtl), cudaMemcpyDeviceToHost, pl->stream), "ctl D2H");
     cuda_check(cudaStreamSynchronize(pl->stream), "ctl sync");
     pl->ctl_valid = true;
+    check_invariants();
 }
 
 double bits_to_cost(uint64_t best) {

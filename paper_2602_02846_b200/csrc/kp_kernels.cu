@@ -120,7 +120,9 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
             if (i < n_items) {
                 const uint32_t f = i / lam;
                 const uint32_t br = i - f * lam;
+                KP_ASSERT(f < ctl->n_va, 10);
                 const uint32_t node = va[f];
+                KP_ASSERT(node < ctl->n_nodes, 11);
                 float u[M], dt;
                 sample_item<M>(P, seed, it, node, br, u, dt);
                 const int S = step_count(P, dt);
@@ -187,6 +189,8 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
             if (rc != 0) continue;
             ++c[0];
             const uint32_t bits = __float_as_uint(o.acc);
+            KP_ASSERT(o.region < P.n_regions, 12);
+            KP_ASSERT(i < S_cap, 13);
             const uint32_t old = atomicMin(B.rc + o.region, bits);
             if (bits > old) continue;  // Worse: discarded (Improved / Equal admitted)
             ++c[1];
@@ -282,8 +286,11 @@ KP_DEV Cnt3 block_scan3(Cnt3 x, Cnt3* total) {
 // Returns the new status; writes status / i_count when they change.
 KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, uint32_t* term, uint32_t* deact,
                           uint32_t* react, uint32_t* hops) {
+    KP_ASSERT(g < P.capacity, 20);
     const uint8_t st = B.status[g];
     const uint32_t a = B.acc[g];
+    KP_ASSERT(B.region[g] < P.n_regions, 21);
+    KP_ASSERT(st != KP_ST_TERMINAL, 22);  // Terminal nodes never stay in the live list
     if (a > B.rc[B.region[g]]) {  // (1) dominated -> Terminal (absorbing)
         B.status[g] = KP_ST_TERMINAL;
         ++*term;
@@ -311,6 +318,8 @@ KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, ui
         for (;;) {
             ++*hops;
             const int32_t q = static_cast<int32_t>(L.x);
+            KP_ASSERT(L.y < P.n_regions, 23);
+            KP_ASSERT(q < static_cast<int32_t>(P.capacity), 24);
             uint4 Ln = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
             if (q >= 0) Ln = B.link[q];
             if (L.z > B.rc[L.y]) { dominated = true; break; }
@@ -441,6 +450,7 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
                 nslot += sl < n_items;
                 if (sl < n_items && ((B.admit_mask[sl >> 5] >> (sl & 31)) & 1u)) {
                     ++nadm;
+                    KP_ASSERT(B.vu_region[sl] < P.n_regions, 25);
                     commit = B.vu_acc[sl] == B.rc[B.vu_region[sl]];  // Alg. 4 line 3, bit-exact
                     x.c = commit;
                 }
@@ -470,6 +480,7 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
                     const uint32_t bit = __fns(aL, 0, static_cast<int>(k - eL) + 1);
                     const uint32_t sl = 32u * wL + bit;
                     ++nadm;
+                    KP_ASSERT(sl < n_items && B.vu_region[sl] < P.n_regions, 26);
                     if (B.vu_acc[sl] == B.rc[B.vu_region[sl]])  // Alg. 4 line 3, bit-exact
                         atomicOr(&s_cm[(threadIdx.x & ~31u) + static_cast<uint32_t>(L)], 1u << bit);
                 }
@@ -483,6 +494,7 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
             }
         }
         const Cnt3 tot = block_sum3(x);
+        KP_ASSERT(tile < B.max_tiles, 27);
         if (threadIdx.x == 0) {
             B.tile_sums[tile] = tot.k;
             B.tile_sums[B.max_tiles + tile] = tot.v;
@@ -534,6 +546,7 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
     const unsigned long long st_att = ctl->stats.attempted, st_com = ctl->stats.committed;
     const unsigned long long st_drop = ctl->stats.dropped_capacity;
     const uint32_t n_live1 = tot_keep + accepted, n_va1 = tot_va + accepted, n_nodes1 = n_nodes + accepted;
+    KP_ASSERT(n_nodes1 <= P.capacity && n_live1 <= n_nodes1 && n_va1 <= n_live1, 40);
     const unsigned long long items = static_cast<unsigned long long>(n_va1) * lam;
     ctl->stats.attempted = st_att + n_items;
     ctl->stats.committed = st_com + accepted;
@@ -664,6 +677,8 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     // one committed slot -> node id n_nodes + rank (slot order), store, lists, best
     auto commit_node = [&](uint32_t sl, uint32_t rank, bool goal) {
         const uint32_t id = n_nodes + rank;
+        KP_ASSERT(id < cap && sl < S && sl / lam < ctl->n_va, 30);
+        KP_ASSERT(tot_keep + rank < cap && tot_va + rank < cap, 31);
 #pragma unroll 4
         for (int d = 0; d < P.n; ++d)
             B.state[static_cast<size_t>(d) * cap + id] = B.vu_state[static_cast<size_t>(d) * S + sl];
@@ -717,6 +732,7 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         run.v += tot.v;
         run.c += tot.c;
         if (x.k) {
+            KP_ASSERT(pk < cap && pv < cap, 32);
             live_n[pk] = g;
             if (x.v) va_n[pv] = g;
         }
@@ -1066,4 +1082,19 @@ cudaError_t launch_reintegrate(const KpProblem& P, const KpBuffers& B, const int
     return cudaGetLastError();
 }
 
+}  // namespace kp
+
+namespace kp {
+// Checks build: first failed device invariant (0 = none), cleared on read.
+cudaError_t read_check_code(unsigned int* code) {
+#ifdef KP_CHECKS
+    cudaError_t e = cudaMemcpyFromSymbol(code, kp_check_code, sizeof(unsigned int));
+    if (e != cudaSuccess) return e;
+    const unsigned int z = 0;
+    return cudaMemcpyToSymbol(kp_check_code, &z, sizeof z);
+#else
+    *code = 0;
+    return cudaSuccess;
+#endif
+}
 }  // namespace kp

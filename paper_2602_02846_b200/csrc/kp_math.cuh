@@ -23,6 +23,11 @@
 
 namespace kp {
 
+#ifdef KP_CHECKS
+__device__ unsigned int kp_check_code;
+__device__ __noinline__ void check_fail(unsigned int code) { atomicCAS(&kp_check_code, 0u, code); }
+#endif
+
 // ------------------------------------------------------------------- RNG ---
 KP_DEV uint64_t mix64(uint64_t z) {  // rng.hpp:34-39
     z += 0x9E3779B97F4A7C15ULL;
@@ -288,10 +293,13 @@ KP_DEV bool in_obstacle(const KpProblem& P, const Env& E, float px, float py, fl
                         uint32_t& nsph) {
     const int c = bg_cell(P, px, 0) + P.bg_n[0] * (bg_cell(P, py, 1) + P.bg_n[1] * bg_cell(P, pz, 2));
     const uint32_t base = E.base;
+    KP_ASSERT(c >= 0 && c < P.n_cells, 1);
     const uint32_t range = lds_u32(base + E.off_cells + 4u * static_cast<uint32_t>(c));
     const int b = static_cast<int>(range & 0xFFFFu), e = static_cast<int>(range >> 16);
+    KP_ASSERT(b <= e && e <= P.n_entries, 2);
     for (int k = b; k < e; ++k) {
         const int id = static_cast<int>(lds_u16(base + E.off_cids + 2u * static_cast<uint32_t>(k)));
+        KP_ASSERT(id < P.n_box + P.n_sph, 3);
         if (id < P.n_box) {
             const float4 lo = lds_f4(base + 16u * static_cast<uint32_t>(id));
             const float4 hi = lds_f4(base + E.off_bhi + 16u * static_cast<uint32_t>(id));

@@ -20,6 +20,21 @@
 #define KP_SELECT_TILE (KP_SELECT_THREADS * KP_SELECT_ITEMS)
 #define KP_SMEM_OBSTACLES 2048
 
+// Device invariant checks (`make checks`: -DKP_CHECKS): index bounds of every
+// indirect access on the iteration's path.  A failed check records its code in
+// kp_check_code (first failure wins) and the host raises after the solve; the
+// product build compiles them out.
+#ifdef KP_CHECKS
+#define KP_ASSERT(cond, code) \
+    do {                      \
+        if (!(cond)) kp::check_fail(code); \
+    } while (0)
+#else
+#define KP_ASSERT(cond, code) \
+    do {                      \
+    } while (0)
+#endif
+
 enum KpStatus : uint8_t { KP_ST_ACTIVE = 0, KP_ST_INACTIVE = 1, KP_ST_TERMINAL = 2 };
 
 struct KpProblem {
