@@ -643,7 +643,10 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         pl->h_ctl = static_cast<KpCtl*>(hc);
         cuda_check(kp::set_propagate_smem(P), "smem attribute");
         const int occ = std::max(1, kp::propagate_occupancy(P));
+        // test hook: KP_PROP_GRID caps the propagate grid, so the multi-group
+        // (lane refill) path runs at small item counts
         pl->grid_prop = pl->sms * occ;
+        if (const char* g = std::getenv("KP_PROP_GRID")) pl->grid_prop = std::max(1, std::min(pl->grid_prop, std::atoi(g)));
         pl->grid_sel = pl->sms * 4;
 
         for (auto*& e : pl->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");

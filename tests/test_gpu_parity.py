@@ -186,3 +186,22 @@ def test_slot_overflow_fails_loudly():
     with Planner(s, seed=1) as g:
         with pytest.raises(KinoplanError, match="max_slots"):
             g.solve(budget_s=0.0, max_iterations=20)
+
+
+@pytest.mark.parametrize("scene,iters", [("forest_di6", 10), ("narrow_dubins6", 8), ("building_quad12", 5),
+                                          ("zigzag2d", 30)])
+def test_whole_run_bit_identical_multi_group(scene, iters, monkeypatch):
+    """A small propagate grid (test hook KP_PROP_GRID) makes every warp run
+    several item groups with lane refill; results stay bit-identical."""
+    monkeypatch.setenv("KP_PROP_GRID", "12")
+    s = scenarios.load(scene)
+    with Planner(s, seed=9) as g:
+        rg = g.solve(budget_s=0.0, max_iterations=iters)
+    monkeypatch.delenv("KP_PROP_GRID")
+    with Planner(s, seed=9) as g2:
+        rg2 = g2.solve(budget_s=0.0, max_iterations=iters)
+        o = kpo.Oracle(s, kpo.MIRROR32, seed=9, workers=8)
+        ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
+        _compare_runs(g2, o, rg2, ro)
+    for k in ("best_cost", "node_count", "propagations_valid", "nodes_committed", "timeline_len"):
+        assert rg[k] == ro[k], (k, rg[k], ro[k])
