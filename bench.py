@@ -130,6 +130,26 @@ def _dist():
     return ws, rank, local
 
 
+def _init_ranks(ws: int, local: int):
+    """One process per GPU (NCCL).  Returns (device index, reduce device): on
+    a box with fewer GPUs than ranks (functional checks only: replicas never
+    wait on each other) ranks share devices and reduce over gloo on the host."""
+    import torch
+
+    ngpu = max(1, torch.cuda.device_count())
+    dev_idx = local % ngpu
+    torch.cuda.set_device(dev_idx)
+    if ws > 1:
+        import torch.distributed as dist
+
+        if ngpu >= ws:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+            return dev_idx, torch.device("cuda", dev_idx)
+        dist.init_process_group("gloo")
+        return dev_idx, torch.device("cpu")
+    return dev_idx, torch.device("cuda", dev_idx)
+
+
 def _median(xs):
     xs = [x for x in xs if x == x]
     return statistics.median(xs) if xs else None
@@ -189,12 +209,7 @@ def run_b200(args, scenario):
     from paper_2602_02846_b200 import Planner, replicas
 
     ws, rank, local = _dist()
-    if ws > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+    local, red_dev = _init_ranks(ws, local)
     dev = torch.device("cuda", local)
     budget = args.budget_ms / 1000.0
     iters = args.iters
@@ -240,7 +255,7 @@ def run_b200(args, scenario):
     prof1 = planner.profile()
     dev_ms = e0.elapsed_time(e1)
     props = sum(r["propagations_attempted"] for r in results)
-    dev_ms, props_total = replicas.reduce_job(dev_ms, props, world=ws, device=dev)
+    dev_ms, props_total = replicas.reduce_job(dev_ms, props, world=ws, device=red_dev)
     results = replicas.gather_results(results, world=ws)
     value = props_total / (dev_ms / 1e3)
 
@@ -264,7 +279,7 @@ def run_b200(args, scenario):
         r = planner.solve(max(budget, 1.0), 0)
         ttfs_wall.append((time.perf_counter() - t0) * 1e3 if r["found"] else float("nan"))
     planner.set_stop_at_first_solution(False)
-    t_e2e, e2e_total = replicas.reduce_job(t_e2e, e2e_props, world=ws, device=dev)
+    t_e2e, e2e_total = replicas.reduce_job(t_e2e, e2e_props, world=ws, device=red_dev)
 
     # ---- per-kernel roofline pass (one query, per-launch CUDA events) ----
     roof = None
@@ -513,11 +528,7 @@ def run_batch(args, scenario):
     from paper_2602_02846_b200 import BatchPlanner, replicas
 
     ws, rank, local = _dist()
-    if ws > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local, red_dev = _init_ranks(ws, local)
     s = json.loads(json.dumps(scenario))
     s["planner"]["capacity"] = 1 << 19
     s["planner"]["max_slots"] = 1 << 21
@@ -532,7 +543,7 @@ def run_batch(args, scenario):
         if ws > 1:
             torch.distributed.barrier()
     props = sum(r["propagations_attempted"] for r in res)
-    wall_max, props_total = replicas.reduce_job(wall * 1e3, props, world=ws, device=torch.device("cuda", local))
+    wall_max, props_total = replicas.reduce_job(wall * 1e3, props, world=ws, device=red_dev)
     res_all = replicas.gather_results(res, world=ws)
     if rank == 0:
         ttfs = [r["first_solution_s"] * 1e3 for r in res_all if r["found"]]
