@@ -393,25 +393,29 @@ def other_configs(args, budget):
             "ms_to_first_solution_median": _median(tt), "success_rate": len(tt) / len(res)}
     except Exception as e:  # noqa: BLE001
         out["batch_" + args.config] = {"error": str(e)[:200]}
-    try:
-        s = scenarios.load("building_quad12")
-        s["planner"]["capacity"] = max(int(s["planner"]["capacity"]), (1 << 22) // 32)
-        s["planner"]["max_slots"] = 1 << 22
-        pk = _peaks()
-        with Planner(s, seed=1) as g:
-            g.sweep(1 << 10, launches=2)
-            rows = []
-            for k in (18, 20, 22):
-                ms, one = g.sweep((1 << k) // 32, launches=3)
-                ops = (one["rk4_steps"] * OPS_PER_STEP["quadcopter_12d"] + one["items"] * OPS_PER_ITEM
-                       + one["box_tests"] * OPS_PER_BOX + one["sphere_tests"] * OPS_PER_SPHERE
-                       + one["interp_points"] * OPS_PER_INTERP)
-                rows.append({"k": k, "items_per_s": one["items"] / (ms * 1e-3),
-                             "frac": ops / (ms * 1e-3) / pk["fp32_lane_ops"]})
-        out["sweep_building_quad12"] = {"kernel": "k_propagate<3>", "bound": "fp32", "peak_src": pk["fp32_src"],
-                                        "rows": rows, "best_frac": max(r["frac"] for r in rows)}
-    except Exception as e:  # noqa: BLE001
-        out["sweep_building_quad12"] = {"error": str(e)[:200]}
+    # propagate throughput sweeps (config 5 on Quad12; the DI6 headline model
+    # beside it shows the same kernel's saturated efficiency)
+    pk = _peaks()
+    for scene, model in (("building_quad12", "quadcopter_12d"), ("forest_di6", "double_integrator_6d")):
+        try:
+            s = scenarios.load(scene)
+            s["planner"]["capacity"] = max(int(s["planner"]["capacity"]), (1 << 22) // 32)
+            s["planner"]["max_slots"] = 1 << 22
+            with Planner(s, seed=1) as g:
+                g.sweep(1 << 10, launches=2)
+                rows = []
+                for k in (18, 20, 22):
+                    ms, one = g.sweep((1 << k) // 32, launches=3)
+                    ops = (one["rk4_steps"] * OPS_PER_STEP[model] + one["items"] * OPS_PER_ITEM
+                           + one["box_tests"] * OPS_PER_BOX + one["sphere_tests"] * OPS_PER_SPHERE
+                           + one["interp_points"] * OPS_PER_INTERP)
+                    rows.append({"k": k, "items_per_s": one["items"] / (ms * 1e-3),
+                                 "frac": ops / (ms * 1e-3) / pk["fp32_lane_ops"]})
+            mi = {"double_integrator_6d": 1, "quadcopter_12d": 3}[model]
+            out["sweep_" + scene] = {"kernel": f"k_propagate<{mi}>", "bound": "fp32", "peak_src": pk["fp32_src"],
+                                     "rows": rows, "best_frac": max(r["frac"] for r in rows)}
+        except Exception as e:  # noqa: BLE001
+            out["sweep_" + scene] = {"error": str(e)[:200]}
     return out
 
 
