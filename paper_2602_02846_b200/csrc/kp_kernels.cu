@@ -91,10 +91,15 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
     const uint32_t n_items = ctl->n_items;
-    // groups per warp: enough that one chunk per block covers the launch (ceil),
-    // so a warp runs G groups back to back instead of a block running 2 chunks
-    const uint32_t G = min(KP_PROP_MAXG, max(1u, (n_items + KP_PROP_THREADS * gridDim.x - 1) / (KP_PROP_THREADS * gridDim.x)));
-    const uint32_t CH = KP_PROP_THREADS * G;
+    // Chunk of slots per block: one block width while the launch fits in one
+    // wave; beyond that, the items are spread evenly over every block (CH a
+    // multiple of 32, so a few warps per block run a second, short group)
+    // instead of doubling the chunk and leaving half the blocks idle.
+    const uint32_t wave = KP_PROP_THREADS * gridDim.x;
+    const uint32_t CH = n_items <= wave
+                            ? KP_PROP_THREADS
+                            : min(KP_PROP_THREADS * KP_PROP_MAXG, ((n_items + gridDim.x - 1) / gridDim.x + 31u) & ~31u);
+    const uint32_t G = (CH + KP_PROP_THREADS - 1) / KP_PROP_THREADS;  // sampling rounds / group rounds
     const uint32_t n_chunks = (n_items + CH - 1) / CH;
     if (blockIdx.x >= n_chunks) return;  // nothing for this block this iteration
     const uint32_t it = ctl->iter;
@@ -117,7 +122,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
             const uint32_t p = k * KP_PROP_THREADS + threadIdx.x;
             const uint32_t i = c0 + p;
             uint32_t key = 0;
-            if (i < n_items) {
+            if (p < CH && i < n_items) {
                 const uint32_t f = i / lam;
                 const uint32_t br = i - f * lam;
                 KP_ASSERT(f < ctl->n_va, 10);
@@ -171,7 +176,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
             const uint32_t pos = (k * NW + wk) * 32 + lane;
             const uint32_t p = sh.perm[pos];
             const uint32_t i = c0 + p;
-            if (i >= n_items) continue;
+            if (p >= CH || i >= n_items) continue;
             const uint32_t node = sh.node[p];
             float x[N], u[M];
 #pragma unroll
