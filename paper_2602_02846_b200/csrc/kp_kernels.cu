@@ -95,10 +95,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     // wave; beyond that, the items are spread evenly over every block (CH a
     // multiple of 32, so a few warps per block run a second, short group)
     // instead of doubling the chunk and leaving half the blocks idle.
-    const uint32_t wave = KP_PROP_THREADS * gridDim.x;
-    const uint32_t CH = n_items <= wave
-                            ? KP_PROP_THREADS
-                            : min(KP_PROP_THREADS * KP_PROP_MAXG, ((n_items + gridDim.x - 1) / gridDim.x + 31u) & ~31u);
+    const uint32_t CH = min(KP_PROP_THREADS * KP_PROP_MAXG, ((n_items + gridDim.x - 1) / gridDim.x + 31u) & ~31u);
     const uint32_t G = (CH + KP_PROP_THREADS - 1) / KP_PROP_THREADS;  // sampling rounds / group rounds
     const uint32_t n_chunks = (n_items + CH - 1) / CH;
     if (blockIdx.x >= n_chunks) return;  // nothing for this block this iteration
