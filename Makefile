@@ -25,7 +25,10 @@ $(CSRC)/kinoplan.o: $(CSRC)/kinoplan.cpp include/kinoplan_b200/kinoplan.hpp incl
 $(CSRC)/bench.o: $(CSRC)/bench.cpp include/kinoplan_b200/bench.hpp include/kinoplan_b200/kinoplan.hpp
 	g++ -std=c++20 -O2 -fPIC -ffp-contract=off -Iinclude -c $< -o $@
 
-$(LIB): $(CSRC)/kp_kernels.o $(CSRC)/kp_capi.o $(CSRC)/kinoplan.o $(CSRC)/bench.o
+$(CSRC)/kinoplan_host.o: $(CSRC)/kinoplan_host.cpp include/kinoplan_b200/kinoplan.hpp
+	g++ -std=c++20 -O2 -fPIC -ffp-contract=off -Iinclude -c $< -o $@
+
+$(LIB): $(CSRC)/kp_kernels.o $(CSRC)/kp_capi.o $(CSRC)/kinoplan.o $(CSRC)/bench.o $(CSRC)/kinoplan_host.o
 	mkdir -p $(PKG)/lib
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static -lrt -lpthread -ldl
 

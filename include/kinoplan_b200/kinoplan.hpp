@@ -12,6 +12,7 @@
 // include/kinoplan_b200.h; planning runs on the GPU only.
 #pragma once
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <map>
@@ -34,6 +35,17 @@ struct ConfigError : std::runtime_error { using std::runtime_error::runtime_erro
 struct GridTooFineError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct InvalidSegmentError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };  // no reference counterpart
+
+[[noreturn]] void invariant_failure(const char* expr, const char* file, int line, const std::string& msg);
+}  // namespace kinoplan
+
+// Internal invariants abort: a bug, not a recoverable condition (errors.hpp:35-48).
+#define KINO_CHECK(cond, msg)                                                         \
+    do {                                                                              \
+        if (!(cond)) ::kinoplan::invariant_failure(#cond, __FILE__, __LINE__, (msg)); \
+    } while (0)
+
+namespace kinoplan {
 
 // ---- types.hpp ----
 using Scalar = double;
@@ -128,6 +140,7 @@ struct Obstacle {
 struct Environment {
     Bounds workspace_bounds;
     std::vector<Obstacle> obstacles;
+    Bounds state_bounds;  // SPEC.md:192 full-state limits (is_state_valid); the planner takes PlanningProblem::state_bounds
 };
 
 // ---- problem / config ----
@@ -222,5 +235,103 @@ private:
 
 /// plan(problem, config): one fresh run with config.seed.
 PlanResult plan(const PlanningProblem& problem, const PlannerConfig& config);
+
+// ---------------------------------------------------------------------------
+// Host (fp64) building blocks of the reference API, for callers that set up,
+// check or replay pieces of a plan on the CPU.  The planner itself runs on the
+// GPU (fp32 recipe); these follow the SPEC in double precision.
+// ---------------------------------------------------------------------------
+
+// ---- rng.hpp:12-57 ----
+class SplitMix64 {
+public:
+    using result_type = uint64_t;
+    explicit constexpr SplitMix64(uint64_t seed) noexcept : state_(seed) {}
+    static constexpr result_type min() noexcept { return 0; }
+    static constexpr result_type max() noexcept { return ~result_type{0}; }
+    constexpr result_type operator()() noexcept {
+        state_ += 0x9E3779B97F4A7C15ULL;
+        uint64_t z = state_;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+
+private:
+    uint64_t state_;
+};
+
+[[nodiscard]] constexpr uint64_t mix64(uint64_t z) noexcept {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+[[nodiscard]] constexpr uint64_t derive_stream(uint64_t seed, uint64_t iteration, uint64_t node_id,
+                                               uint64_t branch) noexcept {
+    uint64_t s = mix64(seed);
+    s = mix64(s ^ iteration);
+    s = mix64(s ^ node_id);
+    s = mix64(s ^ branch);
+    return s;
+}
+
+[[nodiscard]] inline Scalar uniform_unit(SplitMix64& rng) noexcept {
+    return static_cast<Scalar>(rng() >> 11) * 0x1.0p-53;
+}
+
+// ---- dynamics ----
+/// Samples at 0, h, ..., dt (last step shortened), classical RK4 under constant
+/// u, angles wrapped after every step; samples[0] == x bit-exact.  A
+/// non-finite state throws InvalidSegmentError ("propagation diverged").
+[[nodiscard]] std::vector<State> propagate_ode(const State& x, const Control& u, Scalar dt, Scalar h,
+                                               const DynamicsModel& model);
+/// Each axis uniform on [lo, hi] (controls in axis order).
+[[nodiscard]] Control sample_control(SplitMix64& rng, const Bounds& bounds);
+/// Uniform on (0, t_prop].
+[[nodiscard]] Scalar sample_duration(SplitMix64& rng, Scalar t_prop);
+
+// ---- environment ----
+/// Within env.state_bounds (every coordinate, when given) and the workspace
+/// (position dims), outside every closed obstacle.
+[[nodiscard]] bool is_state_valid(const State& x, const Environment& env, const DynamicsModel& model);
+/// Every sample valid, plus the dyadic interior points (spacing <= collision_step)
+/// of consecutive samples farther apart than collision_step obstacle-free.
+[[nodiscard]] bool is_segment_valid(std::span<const State> samples, const Environment& env,
+                                    const DynamicsModel& model, Scalar collision_step);
+/// Environment fragment of a scenario file (keys workspace_bounds,
+/// state_bounds, obstacles); SchemaError names the offending primitive.
+[[nodiscard]] Environment load_environment(const std::string& json_fragment);
+
+// ---- decomposition ----
+enum class UpdateOutcome { Improved, Equal, Worse };
+
+/// Region grid over the decomposed state dims with an atomically updatable
+/// cost table (order-preserving u64 encoding of the fp64 cost, +inf initial).
+class RegionGrid {
+public:
+    std::vector<int> dims;        // decomposed state dims
+    Bounds bounds;                // per decomposed dim
+    std::vector<int> cells;       // cells per dim
+    std::vector<Scalar> side;     // cell widths
+    Scalar delta = 0;             // cell diagonal
+    uint64_t n_regions = 0;
+    RegionGrid() = default;
+    RegionGrid(RegionGrid&&) noexcept = default;
+    RegionGrid& operator=(RegionGrid&&) noexcept = default;
+    std::unique_ptr<std::atomic<uint64_t>[]> table;
+};
+
+/// cells_i = max(1, ceil((hi-lo)_i sqrt(n) / delta)) when delta is given, else
+/// `cells`; GridTooFineError above max_cells (0 = 2^28).
+[[nodiscard]] RegionGrid build_grid(const std::vector<int>& dims, const Bounds& bounds,
+                                    std::optional<Scalar> delta, const std::vector<int>& cells,
+                                    uint64_t max_cells = 0);
+/// clamp(floor((x_d - lo) / side), 0, cells - 1), row-major with dim 0 fastest.
+[[nodiscard]] uint64_t region_index(const State& x, const RegionGrid& grid);
+/// Atomic min via CAS on the encoding; Improved / Equal / Worse vs the old value.
+UpdateOutcome try_update_region_cost(RegionGrid& grid, uint64_t i, Scalar c);
+[[nodiscard]] Scalar region_cost(const RegionGrid& grid, uint64_t i);
 
 }  // namespace kinoplan

@@ -260,7 +260,45 @@ void close_out(std::ofstream& f, const std::string& path) {
     if (!f) throw std::runtime_error(path + ": write failed: " + std::strerror(errno));
 }
 
+// Environment fragment: workspace_bounds, optional
+// state_bounds, obstacles; SchemaError names the offending primitive.
+Environment parse_environment(const Field& env) {
+    Environment e;
+    e.workspace_bounds = env.at("workspace_bounds").bounds();
+    if (e.workspace_bounds.size() < 2 || e.workspace_bounds.size() > 3)
+        env.at("workspace_bounds").bad("expected 2 or 3 intervals");
+    if (auto sb = env.opt("state_bounds")) e.state_bounds = sb->bounds();
+    if (auto obs = env.opt("obstacles")) {
+        for (size_t i = 0; i < obs->size(); ++i) {
+            Field o = obs->idx(i);
+            const std::string& ty = o.at("type").string();
+            Obstacle ob;
+            if (ty == "box") {
+                ob.type = Obstacle::Type::Box;
+                fill_xyz(ob.a, o.at("min").nums(), o.at("min"));
+                fill_xyz(ob.b, o.at("max").nums(), o.at("max"));
+                for (int k = 0; k < 3; ++k)
+                    if (ob.a[k] > ob.b[k]) o.bad("box min > max");
+            } else if (ty == "sphere") {
+                ob.type = Obstacle::Type::Sphere;
+                fill_xyz(ob.a, o.at("center").nums(), o.at("center"));
+                ob.b[0] = o.at("radius").num();
+                if (!(ob.b[0] > 0)) o.at("radius").bad("sphere radius <= 0");
+            } else {
+                o.at("type").bad("unknown obstacle type \"" + ty + "\"");
+            }
+            e.obstacles.push_back(ob);
+        }
+    }
+    return e;
+}
+
 }  // namespace
+
+Environment load_environment(const std::string& json_fragment) {
+    Json root = Reader(json_fragment).parse();
+    return parse_environment(Field{&root, "environment"});
+}
 
 // ---------------------------------------------------------------------------
 // Scenario
@@ -286,30 +324,7 @@ Scenario parse_scenario(const std::string& text, const ScenarioOverrides& ov) {
     }
     const DynamicsModel& md = *s.problem.model;
 
-    Field env = pr.at("environment");
-    s.problem.environment.workspace_bounds = env.at("workspace_bounds").bounds();
-    if (auto obs = env.opt("obstacles")) {
-        for (size_t i = 0; i < obs->size(); ++i) {
-            Field o = obs->idx(i);
-            const std::string& ty = o.at("type").string();
-            Obstacle ob;
-            if (ty == "box") {
-                ob.type = Obstacle::Type::Box;
-                fill_xyz(ob.a, o.at("min").nums(), o.at("min"));
-                fill_xyz(ob.b, o.at("max").nums(), o.at("max"));
-                for (int k = 0; k < 3; ++k)
-                    if (ob.a[k] > ob.b[k]) o.bad("box min > max");
-            } else if (ty == "sphere") {
-                ob.type = Obstacle::Type::Sphere;
-                fill_xyz(ob.a, o.at("center").nums(), o.at("center"));
-                ob.b[0] = o.at("radius").num();
-                if (!(ob.b[0] > 0)) o.at("radius").bad("sphere radius <= 0");
-            } else {
-                o.at("type").bad("unknown obstacle type \"" + ty + "\"");
-            }
-            s.problem.environment.obstacles.push_back(ob);
-        }
-    }
+    s.problem.environment = parse_environment(pr.at("environment"));
     Field xi = pr.at("x_init");
     s.problem.x_init = xi.nums();
     if (static_cast<int>(s.problem.x_init.size()) != md.state_dim())

@@ -27,3 +27,17 @@ def test_cpp_dropin_runs(tmp_path):
     assert out.returncode == 0, (out.returncode, out.stdout, out.stderr)
     found, cost, iters, tcost, nsamp = out.stdout.split()
     assert found == "1" and float(cost) > 12.0 and int(iters) > 10 and float(tcost) == float(cost)
+
+
+def test_cpp_host_api_spec_examples(tmp_path):
+    """Host (fp64) building blocks of the drop-in API against the SPEC examples:
+    propagate_ode, sampling, validity, load_environment, grid, atomic region
+    minimum (tests/cpp/host_api_test.cpp).  CPU only."""
+    exe = str(tmp_path / "host_api")
+    lib = os.path.join(ROOT, "paper_2602_02846_b200", "lib")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-pthread", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "host_api_test.cpp"), "-L", lib, "-lkinoplan_b200",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, (out.stdout, out.stderr)
+    assert out.stdout.startswith("ok ")
