@@ -41,3 +41,21 @@ def test_cpp_host_api_spec_examples(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, (out.stdout, out.stderr)
     assert out.stdout.startswith("ok ")
+
+
+@pytest.mark.gpu
+def test_gpu_solutions_verified_in_fp64(tmp_path):
+    """GPU plans (fp32 recipe) re-checked with the host fp64 API: re-propagated
+    segments land on the stored states within 1e-4, the fp64 samples are valid,
+    and the fp64 path length equals the planner's cost within 1e-4."""
+    exe = str(tmp_path / "verify")
+    lib = os.path.join(ROOT, "paper_2602_02846_b200", "lib")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "verify_solution.cpp"), "-L", lib, "-lkinoplan_b200",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    scen = os.path.join(ROOT, "paper_2602_02846_b200", "scenarios")
+    names = ["forest_di6", "narrow_dubins6", "building_quad12", "zigzag2d", "free2d", "zigzag6d", "building6d"]
+    out = subprocess.run([exe] + [os.path.join(scen, n + ".json") for n in names], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, (out.stdout, out.stderr)
+    assert len(out.stdout.strip().splitlines()) == len(names)
