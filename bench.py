@@ -473,7 +473,8 @@ def roofline(scenario, pa, pb):
         "ops_per_launch": ops_launch, "avg_launch_us": t_prop * 1e6, "launches": n_prop,
         "ops_convention": "FP32 lane-ops of the pinned recipe: FFMA, FADD, FMUL, FSETP, FMNMX, FDIV each = 1",
         "share_of_iteration_time": d["t_propagate_s"] / t_total if t_total else None,
-        "select": {"kernel": "k_select_reduce", "bound": "hbm", "achieved": sel_gbs, "peak": pk["hbm_gbs"],
+        "select": {"kernel": "k_select_reduce", "bound": "latency (L2-resident dependent loads; HBM shown for scale)",
+                   "achieved": sel_gbs, "peak": pk["hbm_gbs"],
                    "unit": "GB/s", "frac": sel_gbs / pk["hbm_gbs"], "avg_launch_us": t_sel * 1e6,
                    "peak_src": pk["hbm_src"],
                    "share_of_iteration_time": d["t_select_s"] / t_total if t_total else None},
