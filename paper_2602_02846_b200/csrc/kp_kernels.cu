@@ -66,17 +66,26 @@ KP_DEV Env stage_env(const KpProblem& P, const KpBuffers& B) {
 // steps (SIMT efficiency) — the result of a slot does not depend on which
 // lane runs it.  Admitted slots write their record and set their admit/goal
 // bit with atomicOr (the consumers zero the words after use).
-#define KP_PROP_THREADS 256
-#define KP_PROP_MAXG 4
+// Propagate block shape per model: 512 threads for the 4D/6D models (a larger
+// step-count sort pool, so a 32-slot group spans fewer step counts), 256 for
+// the register-heavy quadcopter (3 blocks/SM); chunks of at most 1024 slots.
+template <int MODEL>
+struct PropCfg {
+    static constexpr int T = MODEL == 3 ? 256 : 512;  // threads per block
+    static constexpr int MAXG = 1024 / T;             // slot rounds per chunk
+    static constexpr int MIN_BLOCKS = MODEL == 3 ? 3 : 2;
+};
+
+int prop_threads(int model) { return model == 3 ? PropCfg<3>::T : PropCfg<1>::T; }
 #define KP_SORT_BUCKETS 64
 
 template <int MODEL>
 struct PropSmem {
-    float u[Model<MODEL>::M][KP_PROP_THREADS * KP_PROP_MAXG];
-    float dt[KP_PROP_THREADS * KP_PROP_MAXG];
-    uint32_t node[KP_PROP_THREADS * KP_PROP_MAXG];
-    uint16_t steps[KP_PROP_THREADS * KP_PROP_MAXG];
-    uint16_t perm[KP_PROP_THREADS * KP_PROP_MAXG];
+    float u[Model<MODEL>::M][PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];
+    float dt[PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];
+    uint32_t node[PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];
+    uint16_t steps[PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];
+    uint16_t perm[PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];
     uint32_t hist[KP_SORT_BUCKETS];
     uint32_t chunk;
     unsigned long long cnt[6];
@@ -86,6 +95,8 @@ template <int MODEL>
 KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MODEL>& sh, const Env& E) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
+    constexpr uint32_t KP_PROP_THREADS = PropCfg<MODEL>::T;
+    constexpr uint32_t KP_PROP_MAXG = PropCfg<MODEL>::MAXG;
     KpCtl* ctl = B.ctl;
     if (ctl->done) return;
     if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
@@ -237,7 +248,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
 }
 
 template <int MODEL>
-__global__ void __launch_bounds__(KP_PROP_THREADS, (MODEL == 3 ? 3 : 4)) k_propagate(KpProblem P, KpBuffers B) {
+__global__ void __launch_bounds__(PropCfg<MODEL>::T, PropCfg<MODEL>::MIN_BLOCKS) k_propagate(KpProblem P, KpBuffers B) {
     __shared__ PropSmem<MODEL> sh;
     const Env E = stage_env(P, B);  // constant data: overlaps the predecessor's tail
     pdl_wait();
@@ -960,10 +971,10 @@ cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_pr
     cudaError_t e = cudaSuccess;
     if (which & 1) {
         switch (P.model) {
-            case 0: e = launch_k(k_propagate<0>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
-            case 1: e = launch_k(k_propagate<1>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
-            case 2: e = launch_k(k_propagate<2>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
-            default: e = launch_k(k_propagate<3>, grid_prop, KP_PROP_THREADS, smem, st, P, B); break;
+            case 0: e = launch_k(k_propagate<0>, grid_prop, PropCfg<0>::T, smem, st, P, B); break;
+            case 1: e = launch_k(k_propagate<1>, grid_prop, PropCfg<1>::T, smem, st, P, B); break;
+            case 2: e = launch_k(k_propagate<2>, grid_prop, PropCfg<2>::T, smem, st, P, B); break;
+            default: e = launch_k(k_propagate<3>, grid_prop, PropCfg<3>::T, smem, st, P, B); break;
         }
         if (e != cudaSuccess) return e;
     }
@@ -992,10 +1003,10 @@ int propagate_occupancy(const KpProblem& P) {
     int nb = 0;
     const size_t smem = propagate_smem(P);
     switch (P.model) {
-        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<0>, KP_PROP_THREADS, smem); break;
-        case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<1>, KP_PROP_THREADS, smem); break;
-        case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<2>, KP_PROP_THREADS, smem); break;
-        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<3>, KP_PROP_THREADS, smem); break;
+        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<0>, PropCfg<0>::T, smem); break;
+        case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<1>, PropCfg<1>::T, smem); break;
+        case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<2>, PropCfg<2>::T, smem); break;
+        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propagate<3>, PropCfg<3>::T, smem); break;
     }
     return nb;
 }
