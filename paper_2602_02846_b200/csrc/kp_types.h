@@ -15,7 +15,9 @@
 #define KP_MAX_M 4
 #define KP_MAX_GRID 6
 #define KP_TIMELINE_CAP 4096
+#ifndef KP_SELECT_THREADS
 #define KP_SELECT_THREADS 256
+#endif
 #define KP_SELECT_ITEMS 4
 #define KP_SELECT_TILE (KP_SELECT_THREADS * KP_SELECT_ITEMS)
 #define KP_SMEM_OBSTACLES 2048
