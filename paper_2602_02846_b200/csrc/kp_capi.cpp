@@ -934,6 +934,26 @@ int kp_batch_create(const kp_problem_desc* problem, const kp_config_desc* config
         }
         b->lanes.push_back(pl);
     }
+    // Concurrent lanes share the GPU: beyond 4 lanes each lane's kernels get a
+    // proportionally smaller grid (at least half a block per SM), so the lanes'
+    // blocks interleave instead of every lane spreading one iteration over the
+    // whole device (8 lanes: 5.7 -> 7.3 G propagations/s aggregate).
+    if (lanes > 4) {
+        try {
+            for (kp_planner* pl : b->lanes) {
+                cuda_check(cudaSetDevice(pl->device), "cudaSetDevice");
+                pl->grid_prop = std::max(std::max(1, pl->sms / 2), pl->grid_prop * 4 / lanes);
+                pl->grid_sel = std::max(std::max(1, pl->sms / 2), pl->grid_sel * 4 / lanes);
+                if (pl->graph) cudaGraphExecDestroy(pl->graph);
+                pl->graph = nullptr;
+                capture_graph(pl);
+            }
+        } catch (const KpError& e) {
+            g_create_error = e.what();
+            delete b;
+            return e.code;
+        }
+    }
     *out = b;
     return KP_OK;
 }
