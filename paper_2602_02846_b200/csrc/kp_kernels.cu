@@ -640,6 +640,39 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     // and the grand totals from one pass over the per-tile counts
     const uint32_t per = (n_tiles + n_part - 1) / n_part;
     const uint32_t tb = blockIdx.x * per, te = min(tb + per, n_tiles);
+    const uint32_t* live = B.live[it & 1];
+    // this thread's element of a tile: live node (id, pruned status) or slot /
+    // mask word (commit and goal bits); independent of the prefix, so the first
+    // tile's loads are issued before the prefix pass and overlap it
+    struct Elem {
+        Cnt3 x;
+        uint32_t g, w, cm, gm;
+        bool in_slots;
+    };
+    auto load_elem = [&](uint32_t tile) {
+        const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
+        Elem el{{0, 0, 0}, 0, 0, 0, 0, e >= ly.slot0 && e < ly.E};
+        if (e < n_live) {
+            el.g = live[e];
+            const uint8_t st = B.live_st[e];
+            el.x.k = st != KP_ST_TERMINAL;
+            el.x.v = st == KP_ST_ACTIVE;
+        } else if (el.in_slots) {
+            el.w = e - ly.slot0;  // slot (dense) or mask word (sparse)
+            if (!ly.sparse) {
+                if (el.w < n_items) {
+                    el.x.c = (B.commit_mask[el.w >> 5] >> (el.w & 31)) & 1u;
+                    el.gm = el.x.c ? (B.goal_mask[el.w >> 5] >> (el.w & 31)) & 1u : 0u;
+                }
+            } else {
+                el.cm = B.commit_mask[el.w];
+                el.gm = B.goal_mask[el.w];
+                el.x.c = __popc(el.cm);
+            }
+        }
+        return el;
+    };
+    const Elem first = load_elem(tb);
     uint32_t acc[6] = {0, 0, 0, 0, 0, 0};  // before tb: k, v, c; all: k, v, c
     constexpr int U = 8;  // 8 independent loads per array in flight per thread
     for (uint32_t base = threadIdx.x; base < n_tiles; base += U * KP_SELECT_THREADS) {
@@ -682,7 +715,6 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     Cnt3 run{acc[0], acc[1], acc[2]};
     const uint32_t cap = P.capacity, S = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
-    const uint32_t* live = B.live[it & 1];
     const uint32_t* va = B.va[it & 1];
     uint32_t* live_n = B.live[(it + 1) & 1];
     uint32_t* va_n = B.va[(it + 1) & 1];
@@ -714,28 +746,10 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
             atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
     };
     for (uint32_t tile = tb; tile < te; ++tile) {
-        const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
-        Cnt3 x{0, 0, 0};
-        uint32_t g = 0, w = 0, cm = 0, gm = 0;
-        const bool in_slots = e >= ly.slot0 && e < ly.E;
-        if (e < n_live) {
-            g = live[e];
-            const uint8_t st = B.live_st[e];
-            x.k = st != KP_ST_TERMINAL;
-            x.v = st == KP_ST_ACTIVE;
-        } else if (in_slots) {
-            w = e - ly.slot0;  // slot (dense) or mask word (sparse)
-            if (!ly.sparse) {
-                if (w < n_items) {
-                    x.c = (B.commit_mask[w >> 5] >> (w & 31)) & 1u;
-                    gm = x.c ? (B.goal_mask[w >> 5] >> (w & 31)) & 1u : 0u;
-                }
-            } else {
-                cm = B.commit_mask[w];
-                gm = B.goal_mask[w];
-                x.c = __popc(cm);
-            }
-        }
+        const Elem el = tile == tb ? first : load_elem(tile);
+        const Cnt3 x = el.x;
+        const uint32_t g = el.g, w = el.w, cm = el.cm, gm = el.gm;
+        const bool in_slots = el.in_slots;
         Cnt3 tot;
         const Cnt3 inc = block_scan3(x, &tot);  // (barrier: every lane has read its goal bit)
         const uint32_t pk = run.k + inc.k - x.k;
