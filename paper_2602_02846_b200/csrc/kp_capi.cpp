@@ -624,7 +624,6 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         const uint64_t max_e = ((cap + 31) & ~31ull) + S;
         B.max_tiles = static_cast<uint32_t>((max_e + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS);
         B.tile_sums = pl->dalloc<uint32_t>(3ull * B.max_tiles);
-        B.tile_prefix = pl->dalloc<uint32_t>(3ull * B.max_tiles);
         const std::vector<uint8_t> blob = build_env(pl->P, boxes, spheres);
         float4* denv = pl->dalloc<float4>(blob.size() / 16);
         cuda_check(cudaMemcpy(denv, blob.data(), blob.size(), cudaMemcpyHostToDevice), "env H2D");

@@ -848,7 +848,6 @@ __global__ void k_start(KpBuffers B, unsigned long long budget_ns, uint32_t max_
     ctl->deadline_ns = budget_ns ? now + budget_ns : 0ull;
     ctl->max_iter_abs = max_iters ? ctl->iter + max_iters : 0u;
     ctl->stop_first = stop_first;
-    ctl->ticket_a = 0;
     ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
     ctl->n_adm_iter = 0;

@@ -18,9 +18,6 @@
 #ifndef KP_SELECT_THREADS
 #define KP_SELECT_THREADS 256
 #endif
-#define KP_SELECT_ITEMS 4
-#define KP_SELECT_TILE (KP_SELECT_THREADS * KP_SELECT_ITEMS)
-#define KP_SMEM_OBSTACLES 2048
 
 // Device invariant checks (`make checks`: -DKP_CHECKS): index bounds of every
 // indirect access on the iteration's path.  A failed check records its code in
@@ -119,7 +116,7 @@ struct KpCtl {
     // produced by select_reduce for select_scatter
     uint32_t n_tiles;
     uint32_t tot_keep, tot_va, tot_commit, accepted;
-    uint32_t ticket_a, ticket_b;
+    uint32_t ticket_b;        // scatter blocks done (the last one closes the iteration)
     uint32_t prop_cursor;     // dynamic chunk cursor of k_propagate (reset at every boundary)
     uint32_t n_adm_iter;      // slots admitted by this iteration's propagate (reset at every boundary);
                               // selects the select kernels' element layout (per slot / per mask word)
@@ -166,7 +163,6 @@ struct KpBuffers {
     uint32_t* commit_mask;  // [max_slots/32]
     // select scratch
     uint32_t* tile_sums;    // [3][max_tiles] per-tile counts (keep, active, commit)
-    uint32_t* tile_prefix;  // [3][max_tiles] (unused scratch)
     uint32_t max_tiles;
     const float4* env;      // environment blob (see KpProblem)
     KpTraceRec* trace;      // [KP_TRACE_CAP] ring, one record per iteration boundary
