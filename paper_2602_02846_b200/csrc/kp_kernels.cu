@@ -420,7 +420,10 @@ struct SelLayout {
 KP_DEV SelLayout sel_layout(uint32_t n_live, uint32_t n_items, uint32_t n_adm) {
     SelLayout l;
     const uint32_t n_words = (n_items + 31u) >> 5;
-    l.sparse = n_adm <= n_words;  // about one admitted slot per word or fewer: one round per warp
+#ifndef KP_SPARSE_DIV
+#define KP_SPARSE_DIV 1
+#endif
+    l.sparse = n_adm * KP_SPARSE_DIV <= n_words;  // about one admitted slot per word or fewer: one round per warp
     l.slot0 = l.sparse ? n_live : ((n_live + 31u) & ~31u);
     l.E = l.slot0 + (l.sparse ? n_words : 32u * n_words);
     l.n_tiles = (l.E + KP_SELECT_THREADS - 1) / KP_SELECT_THREADS;
