@@ -205,3 +205,15 @@ def test_whole_run_bit_identical_multi_group(scene, iters, monkeypatch):
         _compare_runs(g2, o, rg2, ro)
     for k in ("best_cost", "node_count", "propagations_valid", "nodes_committed", "timeline_len"):
         assert rg[k] == ro[k], (k, rg[k], ro[k])
+
+
+@pytest.mark.parametrize("scene,iters", [("forest_di6", 150), ("narrow_dubins6", 100), ("building_quad12", 40)])
+def test_whole_run_bit_identical_steady_state(scene, iters):
+    """Longer runs: past the growth phase into the steady state (sparse select
+    layout, multi-group propagate chunks, capacity pressure on the frontier)."""
+    s = scenarios.load(scene)
+    with Planner(s, seed=13) as g:
+        rg = g.solve(budget_s=0.0, max_iterations=iters)
+        o = kpo.Oracle(s, kpo.MIRROR32, seed=13, workers=16)
+        ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
+        _compare_runs(g, o, rg, ro)
