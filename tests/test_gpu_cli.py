@@ -104,3 +104,14 @@ def test_infeasible_budget_exits_zero_with_nan(tmp_path):
     assert 'class="empty"' in open(tmp_path / "forest_di6.svg").read()
     p = run("plan", "--scenario", f, "--max-iterations", "2")
     assert json.loads(p.stdout)["success"] is False
+
+
+def test_plan_invalid_start_is_an_error(tmp_path):
+    s = json.load(open(os.path.join(SCEN, "forest_di6.json")))
+    box = s["problem"]["environment"]["obstacles"][0]
+    s["problem"]["x_init"][:3] = [(a + b) / 2 for a, b in zip(box["min"], box["max"])]  # inside a tree
+    f = tmp_path / "bad.json"
+    f.write_text(json.dumps(s))
+    p = subprocess.run([CLI, "plan", "--scenario", str(f), "--max-iterations", "3"], capture_output=True, text=True,
+                       timeout=120)
+    assert p.returncode == 1 and "error" in p.stderr  # InvalidProblemError, not a schema error
