@@ -593,7 +593,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="forest_di6",
-                    choices=["forest_di6", "narrow_dubins6", "building_quad12", "zigzag2d", "free2d"])
+                    help="a bundled scenario name (paper_2602_02846_b200/scenarios/) or a scenario JSON path")
     ap.add_argument("--budget-ms", type=float, default=100.0)
     ap.add_argument("--iters", type=int, default=0, help="fixed iterations per step instead of a time budget "
                                                           "(profiling runs; not the headline workload)")
