@@ -605,12 +605,13 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         B.parent = pl->dalloc<int32_t>(cap);
         B.region = pl->dalloc<uint32_t>(cap);
         B.status = pl->dalloc<uint8_t>(cap);
-        B.live_st = pl->dalloc<uint8_t>(cap);
+        B.live_st = pl->dalloc<uint32_t>(cap);
         B.icnt = pl->dalloc<uint16_t>(cap);
         B.link = pl->dalloc<uint4>(cap);
         B.rc = pl->dalloc<uint32_t>(n_regions);
         for (int i = 0; i < 2; ++i) {
-            B.live[i] = pl->dalloc<uint32_t>(cap);
+            B.live[i] = pl->dalloc<uint4>(cap);
+            B.live_si[i] = pl->dalloc<uint32_t>(cap);
             B.va[i] = pl->dalloc<uint32_t>(cap);
         }
         B.vu_state = pl->dalloc<float>(S * P.n);

@@ -295,22 +295,24 @@ KP_DEV Cnt3 block_scan3(Cnt3 x, Cnt3* total) {
     return inc;
 }
 
-// prune_pass rules for one live node (priorities :434-437).
-// Returns the new status; writes status / i_count when they change.
-KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, uint32_t* term, uint32_t* deact,
-                          uint32_t* react, uint32_t* hops) {
+// prune_pass rules for one live node (priorities :434-437),
+// from its live-list entry rec = {id, region, acc bits, parent} and
+// si = status | i_count << 8.  Returns the new status | i_count << 8 and
+// mirrors status / i_count into the node store.
+KP_DEV uint32_t prune_node(const KpProblem& P, const KpBuffers& B, uint4 rec, uint32_t si, uint32_t* term,
+                           uint32_t* deact, uint32_t* react, uint32_t* hops) {
+    const uint32_t g = rec.x;
     KP_ASSERT(g < P.capacity, 20);
-    const uint8_t st = B.status[g];
-    const uint32_t a = B.acc[g];
-    KP_ASSERT(B.region[g] < P.n_regions, 21);
+    const uint32_t st = si & 0xFFu;
+    KP_ASSERT(rec.y < P.n_regions, 21);
     KP_ASSERT(st != KP_ST_TERMINAL, 22);  // Terminal nodes never stay in the live list
-    if (a > B.rc[B.region[g]]) {  // (1) dominated -> Terminal (absorbing)
+    if (rec.z > B.rc[rec.y]) {  // (1) dominated -> Terminal (absorbing)
         B.status[g] = KP_ST_TERMINAL;
         ++*term;
         return KP_ST_TERMINAL;
     }
     if (st == KP_ST_INACTIVE) {  // (2) inactivity counter, reactivation
-        const uint32_t ic = B.icnt[g] + 1u;
+        const uint32_t ic = (si >> 8) + 1u;
         if (ic > static_cast<uint32_t>(P.i_max)) {
             B.icnt[g] = 0;
             B.status[g] = KP_ST_ACTIVE;
@@ -318,14 +320,14 @@ KP_DEV uint8_t prune_node(const KpProblem& P, const KpBuffers& B, uint32_t g, ui
             return KP_ST_ACTIVE;
         }
         B.icnt[g] = static_cast<uint16_t>(ic);
-        return KP_ST_INACTIVE;
+        return KP_ST_INACTIVE | (ic << 8);
     }
     // (3) Active: some ancestor no longer region-minimal -> Inactive.  The walk
     // is software-pipelined over 16-byte node links: the next hop's link load
     // is issued together with this hop's region-cost load, so the chain costs
     // about one L2 round trip per hop.
     bool dominated = P.deact != 0;
-    int32_t p = B.parent[g];
+    const int32_t p = static_cast<int32_t>(rec.w);
     if (!dominated && p >= 0) {
         uint4 L = B.link[p];  // {parent, region, acc, -}
         for (;;) {
@@ -443,7 +445,8 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
     const uint32_t n_tiles = ly.n_tiles;
     const uint32_t n_part = min(gridDim.x, n_tiles);  // participating blocks
     if (blockIdx.x >= n_part) return;
-    const uint32_t* live = B.live[it & 1];
+    const uint4* live = B.live[it & 1];
+    const uint32_t* live_si = B.live_si[it & 1];
     const int lane = threadIdx.x & 31;
     uint32_t term = 0, deact = 0, react = 0, hops = 0, nlive = 0, nslot = 0, nadm = 0;
     if (threadIdx.x < 7) s_st[threadIdx.x] = 0;
@@ -453,8 +456,9 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
         Cnt3 x{0, 0, 0};
         if (e < n_live) {
             ++nlive;
-            const uint8_t st = prune_node(P, B, live[e], &term, &deact, &react, &hops);
-            B.live_st[e] = st;  // scatter reads it by position, in parallel with live[e]
+            const uint32_t si = prune_node(P, B, live[e], live_si[e], &term, &deact, &react, &hops);
+            B.live_st[e] = si;  // scatter reads it by position, in parallel with live[e]
+            const uint32_t st = si & 0xFFu;
             x.k = st != KP_ST_TERMINAL;
             x.v = st == KP_ST_ACTIVE;
         }
@@ -643,21 +647,23 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     // and the grand totals from one pass over the per-tile counts
     const uint32_t per = (n_tiles + n_part - 1) / n_part;
     const uint32_t tb = blockIdx.x * per, te = min(tb + per, n_tiles);
-    const uint32_t* live = B.live[it & 1];
+    const uint4* live = B.live[it & 1];
     // this thread's element of a tile: live node (id, pruned status) or slot /
     // mask word (commit and goal bits); independent of the prefix, so the first
     // tile's loads are issued before the prefix pass and overlap it
     struct Elem {
         Cnt3 x;
-        uint32_t g, w, cm, gm;
+        uint4 rec;
+        uint32_t si, w, cm, gm;
         bool in_slots;
     };
     auto load_elem = [&](uint32_t tile) {
         const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
-        Elem el{{0, 0, 0}, 0, 0, 0, 0, e >= ly.slot0 && e < ly.E};
+        Elem el{{0, 0, 0}, make_uint4(0u, 0u, 0u, 0u), 0, 0, 0, 0, e >= ly.slot0 && e < ly.E};
         if (e < n_live) {
-            el.g = live[e];
-            const uint8_t st = B.live_st[e];
+            el.rec = live[e];
+            el.si = B.live_st[e];
+            const uint32_t st = el.si & 0xFFu;
             el.x.k = st != KP_ST_TERMINAL;
             el.x.v = st == KP_ST_ACTIVE;
         } else if (el.in_slots) {
@@ -719,7 +725,8 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     const uint32_t cap = P.capacity, S = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
     const uint32_t* va = B.va[it & 1];
-    uint32_t* live_n = B.live[(it + 1) & 1];
+    uint4* live_n = B.live[(it + 1) & 1];
+    uint32_t* live_si_n = B.live_si[(it + 1) & 1];
     uint32_t* va_n = B.va[(it + 1) & 1];
     const int lane = threadIdx.x & 31;
     // one committed slot -> node id n_nodes + rank (slot order), store, lists, best
@@ -743,7 +750,8 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         B.link[id] = make_uint4(par, reg, abits, 0u);
         B.status[id] = KP_ST_ACTIVE;
         B.icnt[id] = 0;
-        live_n[tot_keep + rank] = id;
+        live_n[tot_keep + rank] = make_uint4(id, reg, abits, par);
+        live_si_n[tot_keep + rank] = KP_ST_ACTIVE;
         va_n[tot_va + rank] = id;
         if (goal)  // Alg. 4 lines 5-7
             atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
@@ -751,7 +759,7 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     for (uint32_t tile = tb; tile < te; ++tile) {
         const Elem el = tile == tb ? first : load_elem(tile);
         const Cnt3 x = el.x;
-        const uint32_t g = el.g, w = el.w, cm = el.cm, gm = el.gm;
+        const uint32_t g = el.rec.x, w = el.w, cm = el.cm, gm = el.gm;
         const bool in_slots = el.in_slots;
         Cnt3 tot;
         const Cnt3 inc = block_scan3(x, &tot);  // (barrier: every lane has read its goal bit)
@@ -763,7 +771,8 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         run.c += tot.c;
         if (x.k) {
             KP_ASSERT(pk < cap && pv < cap, 32);
-            live_n[pk] = g;
+            live_n[pk] = el.rec;
+            live_si_n[pk] = el.si;
             if (x.v) va_n[pv] = g;
         }
         if (!ly.sparse) {
@@ -833,7 +842,8 @@ __global__ void k_reset_root(KpProblem P, KpBuffers B, unsigned long long seed) 
     B.status[0] = KP_ST_ACTIVE;
     B.icnt[0] = 0;
     B.rc[r] = 0u;  // DECISION: root region seeded with cost 0 (SPEC.md:425 region dominance)
-    B.live[0][0] = 0;
+    B.live[0][0] = make_uint4(0u, r, 0u, 0xFFFFFFFFu);
+    B.live_si[0][0] = KP_ST_ACTIVE;
     B.va[0][0] = 0;
     ctl->n_live = 1;
     ctl->n_va = 1;

@@ -144,13 +144,16 @@ struct KpBuffers {
     int32_t* parent;
     uint32_t* region;
     uint8_t* status;
-    uint8_t* live_st;    // [capacity] status after this iteration's prune, by live-list position
+    uint32_t* live_st;   // [capacity] status | i_count << 8 after this iteration's prune, by live-list position
     uint16_t* icnt;
     // region table [n_regions], encoded fp32 bits (+inf = 0x7F800000)
     uint32_t* rc;
     uint4* link;         // [capacity] {parent, region, acc bits, 0}: one 16-byte load per ancestor hop
     // lists, double-buffered [2][capacity]
-    uint32_t* live[2];
+    // live list entries carry what the prune pass needs (no gathers by id):
+    // {id, region, acc bits, parent} and status | i_count << 8
+    uint4* live[2];
+    uint32_t* live_si[2];
     uint32_t* va[2];
     // V_U slots, SoA [dim][max_slots]
     float* vu_state;
