@@ -98,10 +98,12 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     constexpr uint32_t KP_PROP_THREADS = PropCfg<MODEL>::T;
     constexpr uint32_t KP_PROP_MAXG = PropCfg<MODEL>::MAXG;
     KpCtl* ctl = B.ctl;
-    if (ctl->done) return;
+    // every control-block read up front: one round trip, not one per early exit
+    const uint32_t done = ctl->done, n_items = ctl->n_items, it = ctl->iter;
+    const unsigned long long seed = ctl->seed;
+    if (done) return;
     if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
-    const uint32_t n_items = ctl->n_items;
     // Chunk of slots per block: one block width while the launch fits in one
     // wave; beyond that, the items are spread evenly over every block (CH a
     // multiple of 32, so a few warps per block run a second, short group)
@@ -110,8 +112,6 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     const uint32_t G = (CH + KP_PROP_THREADS - 1) / KP_PROP_THREADS;  // sampling rounds / group rounds
     const uint32_t n_chunks = (n_items + CH - 1) / CH;
     if (blockIdx.x >= n_chunks) return;  // nothing for this block this iteration
-    const uint32_t it = ctl->iter;
-    const unsigned long long seed = ctl->seed;
     const uint32_t* va = B.va[it & 1];
     const uint32_t cap = P.capacity, S_cap = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
@@ -434,14 +434,14 @@ KP_DEV SelLayout sel_layout(uint32_t n_live, uint32_t n_items, uint32_t n_adm) {
 
 KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
     KpCtl* ctl = B.ctl;
-    if (ctl->done) return;
+    // every control-block read up front: one round trip
+    const uint32_t done = ctl->done, it = ctl->iter, n_live = ctl->n_live, n_items = ctl->n_items;
+    const uint32_t n_adm = ctl->n_adm_iter;
+    if (done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_sel_ns = globaltimer();
     __shared__ uint32_t s_st[7];
     __shared__ uint32_t s_cm[KP_SELECT_THREADS];  // commit words under construction (sparse layout)
-    const uint32_t it = ctl->iter;
-    const uint32_t n_live = ctl->n_live;
-    const uint32_t n_items = ctl->n_items;
-    const SelLayout ly = sel_layout(n_live, n_items, ctl->n_adm_iter);
+    const SelLayout ly = sel_layout(n_live, n_items, n_adm);
     const uint32_t n_tiles = ly.n_tiles;
     const uint32_t n_part = min(gridDim.x, n_tiles);  // participating blocks
     if (blockIdx.x >= n_part) return;
@@ -632,14 +632,14 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
 
 KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     KpCtl* ctl = B.ctl;
-    if (ctl->done) return;
+    // every control-block read up front: one round trip
+    const uint32_t done = ctl->done, it = ctl->iter, n_live = ctl->n_live, n_items = ctl->n_items;
+    const uint32_t n_adm = ctl->n_adm_iter, n_nodes = ctl->n_nodes;
+    if (done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_scat_ns = globaltimer();
     __shared__ unsigned int s_last;
     __shared__ uint32_t s_red[6][KP_SELECT_THREADS / 32];
-    const uint32_t it = ctl->iter;
-    const uint32_t n_live = ctl->n_live;
-    const uint32_t n_items = ctl->n_items;
-    const SelLayout ly = sel_layout(n_live, n_items, ctl->n_adm_iter);  // as select_reduce
+    const SelLayout ly = sel_layout(n_live, n_items, n_adm);  // as select_reduce
     const uint32_t n_tiles = ly.n_tiles;
     const uint32_t n_part = min(gridDim.x, n_tiles);
     if (blockIdx.x >= n_part) return;
@@ -718,7 +718,6 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         }
     }
     const uint32_t tot_keep = acc[3], tot_va = acc[4], tot_commit = acc[5];
-    const uint32_t n_nodes = ctl->n_nodes;
     const uint32_t remaining = P.capacity - n_nodes;
     const uint32_t accepted = tot_commit < remaining ? tot_commit : remaining;
     Cnt3 run{acc[0], acc[1], acc[2]};
