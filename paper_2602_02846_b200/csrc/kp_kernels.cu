@@ -74,6 +74,15 @@ struct PropCfg {
     static constexpr int T = MODEL == 3 ? 256 : 512;  // threads per block
     static constexpr int MAXG = 1024 / T;             // slot rounds per chunk
     static constexpr int MIN_BLOCKS = MODEL == 3 ? 3 : 2;
+    // Steps of the first pass of a split rollout (0: never split).  Only the
+    // quadcopter splits: ~55 % of its items stop early (invalid), and a first
+    // pass of 8 steps cuts its warp-steps by ~22 % (scripts/split_sim.py); for
+    // the 4D/6D models the split measured slower (profiles/README.md).
+#ifdef KP_SPLIT_Q
+    static constexpr int SPLIT = MODEL == 3 ? KP_SPLIT_Q : KP_SPLIT_D;
+#else
+    static constexpr int SPLIT = MODEL == 3 ? 8 : 0;
+#endif
 };
 
 int prop_threads(int model) { return model == 3 ? PropCfg<3>::T : PropCfg<1>::T; }
@@ -86,7 +95,11 @@ struct PropSmem {
     uint32_t node[PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];
     uint16_t steps[PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];
     uint16_t perm[PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];
+    uint16_t slist[PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];  // survivors of the first pass (sorted positions)
     uint32_t hist[KP_SORT_BUCKETS];
+    uint32_t gmask[32];  // per 32-slot group: lanes still running after the first pass
+    uint32_t gbase[32];
+    uint32_t n_surv, claim;
     uint32_t chunk;
     unsigned long long cnt[6];
 };
@@ -99,7 +112,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     constexpr uint32_t KP_PROP_MAXG = PropCfg<MODEL>::MAXG;
     KpCtl* ctl = B.ctl;
     // every control-block read up front: one round trip, not one per early exit
-    const uint32_t done = ctl->done, n_items = ctl->n_items, it = ctl->iter;
+    const uint32_t done = ctl->done, n_items = ctl->n_items, it = ctl->iter, split_on = ctl->split;
     const unsigned long long seed = ctl->seed;
     if (done) return;
     if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
@@ -173,49 +186,131 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
             sh.perm[pos] = static_cast<uint16_t>(p);
         }
         __syncthreads();
-        // (3) integrate groups of 32 consecutive sorted slots per warp
-        for (uint32_t k = 0; k < G; ++k) {
-            // snake assignment of the step-sorted groups: round k even hands the
-            // longest groups to the highest warp ids (the arbiter issues highest
-            // warp id first), odd rounds reverse, so each warp's total step count
-            // over its G groups is about the same
-            constexpr uint32_t NW = KP_PROP_THREADS / 32;
-            const uint32_t wk = (k & 1u) ? static_cast<uint32_t>(warp) : NW - 1 - static_cast<uint32_t>(warp);
-            const uint32_t pos = (k * NW + wk) * 32 + lane;
+        // (3) integrate groups of 32 consecutive sorted slots per warp.  When a
+        // warp has several groups (the launch spans more than one wave) and at
+        // least a quarter of the previous iteration's rollouts were invalid, the
+        // rollout is split: every slot first runs at most SPLIT steps; the slots
+        // still running (state + path length parked in this block's scratch) are
+        // compacted in sorted order and finished in full groups claimed longest
+        // first, so the lanes of items that stop early (invalid) do not idle
+        // until the end of a group.  Bit-identical to one pass (integrate_steps).
+        constexpr uint32_t NW = KP_PROP_THREADS / 32;
+        constexpr uint32_t SCR = KP_PROP_THREADS * KP_PROP_MAXG;  // scratch stride (slots per chunk)
+        constexpr int SPLIT = PropCfg<MODEL>::SPLIT;
+        const bool split = SPLIT > 0 && G >= 2 && split_on;
+        float* const scr = B.prop_scratch + static_cast<size_t>(blockIdx.x) * (N + 1) * SCR;
+        uint32_t n_surv = 0;
+        for (uint32_t job = 0;; ++job) {
+            if (job == G) {
+                if (!split) break;
+                // compact the survivors of the first pass (sorted order kept)
+                __syncthreads();
+                if (warp == 0) {
+                    const uint32_t v = lane < G * NW ? __popc(sh.gmask[lane]) : 0u;
+                    uint32_t x = v;
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+                        if (lane >= off) x += y;
+                    }
+                    sh.gbase[lane] = x - v;
+                    if (lane == 31) {
+                        sh.n_surv = x;
+                        sh.claim = 0;
+                    }
+                }
+                __syncthreads();
+                for (uint32_t g = warp; g < G * NW; g += NW) {
+                    const uint32_t m = sh.gmask[g];
+                    if ((m >> lane) & 1u) sh.slist[sh.gbase[g] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(g * 32 + lane);
+                }
+                __syncthreads();
+                n_surv = sh.n_surv;
+            }
+            const bool resume = job >= G;  // second pass: a compacted survivor
+            uint32_t k = job, wk = 0, q;
+            if (!resume) {
+                // snake assignment of the step-sorted groups: round k even hands the
+                // longest groups to the highest warp ids (the arbiter issues highest
+                // warp id first), odd rounds reverse, so each warp's total step count
+                // over its groups is about the same
+                wk = (k & 1u) ? static_cast<uint32_t>(warp) : NW - 1 - static_cast<uint32_t>(warp);
+                q = (k * NW + wk) * 32 + lane;
+            } else {
+                // second pass: warps claim the compacted groups longest first
+                uint32_t g = 0;
+                if (lane == 0) g = atomicAdd(&sh.claim, 1u);
+                g = __shfl_sync(0xFFFFFFFFu, g, 0);
+                if (g * 32 >= n_surv) break;
+                q = g * 32 + lane;
+            }
+            uint32_t pos = q;
+            bool have;
+            if (resume) {
+                have = q < n_surv;
+                pos = have ? sh.slist[q] : 0u;
+            }
             const uint32_t p = sh.perm[pos];
             const uint32_t i = c0 + p;
-            if (p >= CH || i >= n_items) continue;
-            const uint32_t node = sh.node[p];
-            float x[N], u[M];
+            if (!resume) have = p < CH && i < n_items;
+            // loads guarded by `have`; the rollout below is warp-uniform control flow
+            const uint32_t node = have ? sh.node[p] : 0u;
+            const int S = have ? sh.steps[p] : 0;
+            float x[N], u[M], total = 0.0f;
+            if (have) {
+                if (resume) {
 #pragma unroll
-            for (int d = 0; d < N; ++d) x[d] = B.state[static_cast<size_t>(d) * cap + node];
+                    for (int d = 0; d < N; ++d) x[d] = scr[d * SCR + pos];
+                    total = scr[N * SCR + pos];
+                } else {
+#pragma unroll
+                    for (int d = 0; d < N; ++d) x[d] = B.state[static_cast<size_t>(d) * cap + node];
+                }
+            }
 #pragma unroll
             for (int d = 0; d < M; ++d) u[d] = sh.u[d][p];
             const float dt = sh.dt[p];
-            const float acc_p = __uint_as_float(B.acc[node]);
             ItemOut o;
-            const int rc = integrate_item<MODEL>(P, E, x, u, dt, sh.steps[p], acc_p, o);
+            o.steps = o.interp = o.nbox = o.nsph = 0;
+            const int s0 = resume ? SPLIT : 0;
+            const int s1 = (split && !resume) ? min(S, SPLIT) : S;
+            int rc = 1;
+            if (have) rc = integrate_steps<MODEL>(P, E, x, u, dt, S, s0, s1, total, o);
+            const bool running = rc == 0 && s1 < S;
+            const bool ok = rc == 0 && s1 >= S;
             c[2] += o.steps;
             c[3] += o.interp;
             c[4] += o.nbox;
             c[5] += o.nsph;
-            if (rc != 0) continue;
-            ++c[0];
-            const uint32_t bits = __float_as_uint(o.acc);
-            KP_ASSERT(o.region < P.n_regions, 12);
-            KP_ASSERT(i < S_cap, 13);
-            const uint32_t old = atomicMin(B.rc + o.region, bits);
-            if (bits > old) continue;  // Worse: discarded (Improved / Equal admitted)
-            ++c[1];
+            if (running) {  // park it for the second pass
 #pragma unroll
-            for (int d = 0; d < N; ++d) B.vu_state[static_cast<size_t>(d) * S_cap + i] = x[d];
+                for (int d = 0; d < N; ++d) scr[d * SCR + pos] = x[d];
+                scr[N * SCR + pos] = total;
+            }
+            if (split && !resume) {
+                const uint32_t m = __ballot_sync(0xFFFFFFFFu, running);
+                if (lane == 0) sh.gmask[k * NW + wk] = m;
+            }
+            if (ok) {
+                finish_item<MODEL>(P, x, dt, total, __uint_as_float(B.acc[node]), o);
+                ++c[0];
+                const uint32_t bits = __float_as_uint(o.acc);
+                KP_ASSERT(o.region < P.n_regions, 12);
+                KP_ASSERT(i < S_cap, 13);
+                const uint32_t old = atomicMin(B.rc + o.region, bits);
+                if (bits <= old) {  // Improved / Equal admitted, Worse discarded
+                    ++c[1];
 #pragma unroll
-            for (int d = 0; d < M; ++d) B.vu_ctrl[static_cast<size_t>(d) * S_cap + i] = u[d];
-            B.vu_dt[i] = dt;
-            B.vu_acc[i] = bits;
-            B.vu_region[i] = o.region;
-            atomicOr(B.admit_mask + (i >> 5), 1u << (i & 31));
-            if (o.goal) atomicOr(B.goal_mask + (i >> 5), 1u << (i & 31));
+                    for (int d = 0; d < N; ++d) B.vu_state[static_cast<size_t>(d) * S_cap + i] = x[d];
+#pragma unroll
+                    for (int d = 0; d < M; ++d) B.vu_ctrl[static_cast<size_t>(d) * S_cap + i] = u[d];
+                    B.vu_dt[i] = dt;
+                    B.vu_acc[i] = bits;
+                    B.vu_region[i] = o.region;
+                    atomicOr(B.admit_mask + (i >> 5), 1u << (i & 31));
+                    if (o.goal) atomicOr(B.goal_mask + (i >> 5), 1u << (i & 31));
+                }
+            }
         }
         if (n_chunks <= gridDim.x) break;  // every chunk was assigned statically
         __syncthreads();
@@ -235,7 +330,10 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (sh.cnt[0]) atomicAdd(&ctl->stats.valid, sh.cnt[0]);
+        if (sh.cnt[0]) {
+            atomicAdd(&ctl->stats.valid, sh.cnt[0]);
+            atomicAdd(&ctl->n_valid_iter, static_cast<uint32_t>(sh.cnt[0]));
+        }
         if (sh.cnt[1]) {
             atomicAdd(&ctl->stats.admitted, sh.cnt[1]);
             atomicAdd(&ctl->n_adm_iter, static_cast<uint32_t>(sh.cnt[1]));
@@ -565,6 +663,7 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
     const uint32_t max_iter_abs = ctl->max_iter_abs, stop_first = ctl->stop_first;
     const unsigned long long st_att = ctl->stats.attempted, st_com = ctl->stats.committed;
     const unsigned long long st_drop = ctl->stats.dropped_capacity;
+    const uint32_t n_valid = ctl->n_valid_iter;
     const uint32_t n_live1 = tot_keep + accepted, n_va1 = tot_va + accepted, n_nodes1 = n_nodes + accepted;
     KP_ASSERT(n_nodes1 <= P.capacity && n_live1 <= n_nodes1 && n_va1 <= n_live1, 40);
     const unsigned long long items = static_cast<unsigned long long>(n_va1) * lam;
@@ -623,6 +722,10 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
     ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
     ctl->n_adm_iter = 0;
+    ctl->n_valid_iter = 0;
+    // split the next propagate's rollouts when many items stop early (invalid):
+    // the compaction then pays for its second pass (scripts/split_sim.py)
+    ctl->split = (n_items - min(n_valid, n_items)) * 4u >= n_items && n_items > 0 ? 1u : 0u;
     if (done) {
         ctl->done = 1;
         __threadfence_system();
@@ -1085,6 +1188,8 @@ __global__ void k_sweep_prepare(KpProblem P, KpBuffers B, uint32_t n) {
         c->n_items = n * static_cast<uint32_t>(P.lambda);
         c->prop_cursor = 0;
         c->n_adm_iter = 0;
+        c->n_valid_iter = 0;
+        c->split = 0;  // no previous iteration to measure the invalid share on
         c->stats = KpStats{};
     }
 }

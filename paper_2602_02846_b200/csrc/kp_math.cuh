@@ -393,22 +393,19 @@ struct ItemOut {
 // Rollout + validity + cost of one work item whose (u, dt) are drawn (Alg. 2
 // lines 4-7): RK4 rollout streamed in registers, every
 // sample validated and every interpolated point (spacing <= collision_step)
-// obstacle-checked, path length accumulated, region of the end state.  x holds
-// the parent state on entry and the candidate state on a valid exit.  Returns
-// 0 valid, 1 invalid, 2 diverged.  The parent (samples[0]) is not re-checked:
-// it is a stored valid node.
+// obstacle-checked, path length accumulated.  integrate_steps runs steps
+// [s0, s1) of an item with S steps: x holds the state after step s0 on entry
+// (the parent state for s0 = 0) and after the last step run on return, total
+// the path length so far.  Returns 0 (no violation up to s1), 1 invalid,
+// 2 diverged.  The parent (samples[0]) is not re-checked: it is a stored valid
+// node.  Splitting [0, S) at any step is bit-identical to one call.
 template <int MODEL>
-KP_DEV int integrate_item(const KpProblem& P, const Env& E, float* x, const float* u, float dt, int S, float acc_parent,
-                          ItemOut& o) {
+KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const float* u, float dt, int S, int s0, int s1,
+                           float& total, ItemOut& o) {
     constexpr bool TWO_D = (MODEL == 0);
     float px = x[0], py = x[1], pz = TWO_D ? 0.0f : x[2];
-    float total = 0.0f;
-    o.steps = 0;
-    o.interp = 0;
-    o.nbox = 0;
-    o.nsph = 0;
     const float h6 = P.h / 6.0f;
-    for (int s = 0; s < S; ++s) {
+    for (int s = s0; s < s1; ++s) {
         float hk = P.h, sixth = h6;
         if (s + 1 == S) {  // the shortened last step: only here the IEEE division
             hk = dt - static_cast<float>(S - 1) * P.h;
@@ -449,13 +446,32 @@ KP_DEV int integrate_item(const KpProblem& P, const Env& E, float* x, const floa
         total += d;  // cost.hpp:59-61 (position head == workspace dims for every built-in model)
         px = nx; py = ny; pz = nz;
     }
+    return 0;
+}
+
+// Cost, region and goal flag of a valid end state x (Alg. 2 line 7).
+template <int MODEL>
+KP_DEV void finish_item(const KpProblem& P, const float* x, float dt, float total, float acc_parent, ItemOut& o) {
     float seg;
     if (P.cost_kind == 1) seg = dt;                        // control_duration
     else seg = (total == 0.0f) ? P.zero_rate * dt : total;  // cost.hpp:62
     o.acc = acc_parent + seg;
     o.region = region_index<Model<MODEL>::N>(P, x);
     o.goal = in_goal<Model<MODEL>::N>(P, x);
-    return 0;
+}
+
+// A whole rollout: 0 valid (o.acc / o.region / o.goal set), 1 invalid, 2 diverged.
+template <int MODEL>
+KP_DEV int integrate_item(const KpProblem& P, const Env& E, float* x, const float* u, float dt, int S, float acc_parent,
+                          ItemOut& o) {
+    o.steps = 0;
+    o.interp = 0;
+    o.nbox = 0;
+    o.nsph = 0;
+    float total = 0.0f;
+    const int rc = integrate_steps<MODEL>(P, E, x, u, dt, S, 0, S, total, o);
+    if (rc == 0) finish_item<MODEL>(P, x, dt, total, acc_parent, o);
+    return rc;
 }
 
 // One whole work item of Alg. 2 lines 3-7: sample (u, dt), then integrate.

@@ -120,6 +120,8 @@ struct KpCtl {
     uint32_t prop_cursor;     // dynamic chunk cursor of k_propagate (reset at every boundary)
     uint32_t n_adm_iter;      // slots admitted by this iteration's propagate (reset at every boundary);
                               // selects the select kernels' element layout (per slot / per mask word)
+    uint32_t n_valid_iter;    // valid rollouts of this iteration's propagate (reset at every boundary)
+    uint32_t split;           // 1: the next propagate splits its rollouts (>= 1/4 of the last iteration's were invalid)
     // run bookkeeping
     uint32_t max_iter_abs;    // stop when iter >= this (0 = unlimited)
     uint32_t stop_first;
@@ -167,6 +169,7 @@ struct KpBuffers {
     // select scratch
     uint32_t* tile_sums;    // [3][max_tiles] per-tile counts (keep, active, commit)
     uint32_t max_tiles;
+    float* prop_scratch;    // [propagate grid][n + 1][1024]: per-block parked rollouts (state, path length)
     const float4* env;      // environment blob (see KpProblem)
     KpTraceRec* trace;      // [KP_TRACE_CAP] ring, one record per iteration boundary
     float* x0;              // [KP_MAX_N] current query's start state (H2D per query)

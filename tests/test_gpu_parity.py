@@ -192,7 +192,8 @@ def test_slot_overflow_fails_loudly():
                                           ("zigzag2d", 30)])
 def test_whole_run_bit_identical_multi_group(scene, iters, monkeypatch):
     """A small propagate grid (test hook KP_PROP_GRID) makes every warp run
-    several item groups with lane refill; results stay bit-identical."""
+    several item groups (and the quadcopter's rollouts split into two passes
+    with compaction in between); results stay bit-identical."""
     monkeypatch.setenv("KP_PROP_GRID", "12")
     s = scenarios.load(scene)
     with Planner(s, seed=9) as g:
