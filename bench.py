@@ -308,13 +308,44 @@ def run_b200(args, scenario):
             if r["found"]:
                 ttfs.append(r["first_solution_s"] * 1e3)
                 costs.append(r["best_cost"])
+        # deterministic mode (workers = 1) beside it: a shorter sample
+        p1, w1 = 0, 0.0
+        for sd in qs[:max(1, n_q // 2)]:
+            r = cpu_planner_run(scenario, sd, args.cpu_query_s, 1, False)
+            p1 += r["propagations_attempted"]
+            w1 += r["wall_s"]
         cpu = {"value": props / wall, "unit": "propagations/s", "cores": cores, "kind": "port",
                "sample": f"{args.config}, {n_q} queries (seeds {qs[0]}..{qs[-1]}) "
                          f"x {args.cpu_query_s:g} s budget each on {cores} threads, fp64 restatement "
                          "(oracle Faithful64, SplitMix64)",
                "wall_s": wall,
                "ms_to_first_solution_median": _median(ttfs), "solution_cost_at_budget_median": _median(costs),
-               "success_rate": len(ttfs) / n_q}
+               "success_rate": len(ttfs) / n_q,
+               "single_thread": {"value": p1 / w1, "unit": "propagations/s", "cores": 1,
+                                 "sample": f"{max(1, n_q // 2)} queries x {args.cpu_query_s:g} s, workers = 1"}}
+
+    dist = None
+    if rank == 0 and args.dist_seeds > 0:
+        # BASELINE metrics as distributions over seeds 0..N-1:
+        # time to first solution (stop-at-first queries) and cost at the budget
+        tt, costs_d, found = [], [], 0
+        planner.set_stop_at_first_solution(True)
+        for sd in range(args.dist_seeds):
+            planner.reset(sd, x_init=x_init)
+            r = planner.solve(max(budget, 1.0), 0)
+            if r["found"]:
+                tt.append(r["first_solution_s"] * 1e3)
+        planner.set_stop_at_first_solution(False)
+        for sd in range(args.dist_seeds):
+            planner.reset(sd, x_init=x_init)
+            r = planner.solve(budget, iters)
+            if r["found"]:
+                found += 1
+                costs_d.append(r["best_cost"])
+        dist = {"seeds": [0, args.dist_seeds - 1],
+                "ms_to_first_solution_median": _median(tt), "ms_to_first_solution_p25_p75": _quart(tt),
+                "solution_cost_at_budget_median": _median(costs_d), "solution_cost_at_budget_p25_p75": _quart(costs_d),
+                "success_rate": found / args.dist_seeds}
 
     extras = {}
     if rank == 0 and ws == 1 and not args.no_extras:
@@ -345,6 +376,7 @@ def run_b200(args, scenario):
                 "node_propagations_per_sec": value,
                 "iterations_median": _median([r["iterations"] for r in results]),
                 "capacity_exhausted_steps": sum(r["capacity_exhausted"] for r in results),
+                "over_seeds": dist,
             },
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -599,6 +631,8 @@ def main():
                                                           "(profiling runs; not the headline workload)")
     ap.add_argument("--seed-base", type=int, default=1000)
     ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="CPU baseline sample: total seconds")
+    ap.add_argument("--dist-seeds", type=int, default=100,
+                    help="seeds 0..N-1 for the TTFS / cost distributions (untimed; 0 = skip)")
     ap.add_argument("--cpu-query-s", type=float, default=2.5, help="CPU baseline sample: budget per query")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the other-config summaries")
