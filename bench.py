@@ -59,11 +59,14 @@ def _peaks():
 # FMNMX, FRND, FDIV, FSQRT each = 1), per unit of device work counted by
 # kp_profile.  Per RK4 step: 3N stage FMAs + 4N combine + 1 (h/2)
 # + 2N bound compares + distance (7 in 3-D, 5 in 2-D) + 1 cost add + 4
-# derivative evaluations (+2 per wrapped angle).  sincos recipe = 15.
+# derivative evaluations (+2 per wrapped angle).  sincos recipe = 15.  The
+# double integrator's samples are closed-form: t and t*t, then
+# per position dim u/2 and two FMAs, per velocity dim one FMA; + bounds,
+# distance and cost add as above.
 _SINCOS = 15
 OPS_PER_STEP = {
-    "double_integrator_4d": 3 * 4 + 4 * 4 + 1 + 8 + 5 + 1,                       # 43
-    "double_integrator_6d": 3 * 6 + 4 * 6 + 1 + 12 + 7 + 1,                      # 63
+    "double_integrator_4d": 2 + 2 * 4 + 8 + 5 + 1,                               # 24
+    "double_integrator_6d": 2 + 3 * 4 + 12 + 7 + 1,                              # 34
     "dubins_airplane_6d": 3 * 6 + 4 * 6 + 1 + 12 + 7 + 1 + 2 + 4 * (2 * _SINCOS + 4),   # 201
     "quadcopter_12d": 3 * 12 + 4 * 12 + 1 + 24 + 7 + 1 + 6 + 4 * (3 * _SINCOS + 26),   # 407
 }

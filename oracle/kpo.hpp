@@ -135,6 +135,7 @@ struct Faithful64 {
     using R = double;
     using Enc = uint64_t;
     static R madd(R a, R b, R c) { return a * b + c; }  // two roundings (-ffp-contract=off)
+    static constexpr bool kClosedFormDI = false;         // the reference's RK4 for every model
     static void sincos(R x, R* s, R* c) { *s = std::sin(x); *c = std::cos(x); }
     static Enc encode(R v) { Enc e; std::memcpy(&e, &v, sizeof e); return e; }
     static R decode(Enc e) { R v; std::memcpy(&v, &e, sizeof v); return v; }
@@ -145,6 +146,7 @@ struct Mirror32 {
     using R = float;
     using Enc = uint32_t;
     static R madd(R a, R b, R c) { return std::fma(a, b, c); }
+    static constexpr bool kClosedFormDI = true;  // device recipe: double integrator in closed form
     static void sincos(R x, R* s, R* c) { sincos_recipe_f32(x, s, c); }
     static Enc encode(R v) { Enc e; std::memcpy(&e, &v, sizeof e); return e; }
     static R decode(Enc e) { R v; std::memcpy(&v, &e, sizeof v); return v; }
@@ -391,6 +393,33 @@ bool propagate_ode(const ProblemDef& pd, const Consts<P>& k, const Vec<typename 
     const R q = dt / h;
     int S = static_cast<int>(std::ceil(q));
     if (S < 1) S = 1;
+    if constexpr (P::kClosedFormDI) {
+        if (pd.model == ModelId::DI4 || pd.model == ModelId::DI6) {
+            // RK4 with constant control is exact on the double integrator
+            // (SPEC.md:138-139): the device evaluates every sample in closed
+            // form from x0, p = MADD(u/2, t*t, MADD(v0, t, p0)), v = MADD(u, t, v0),
+            // t = (s+1) h, the last sample at dt (skipped when dt - (S-1) h <= 0)
+            const int D = n / 2;
+            Vec<R> x;
+            x.n = n;
+            for (int s = 0; s < S; ++s) {
+                R t = R(s + 1) * h;
+                if (s + 1 == S) {
+                    if (!(dt - R(S - 1) * h > R(0))) break;
+                    t = dt;
+                }
+                const R tt = t * t;
+                for (int i = 0; i < D; ++i) {
+                    x[i] = P::madd(R(0.5) * u[i], tt, P::madd(x0[D + i], t, x0[i]));
+                    x[D + i] = P::madd(u[i], t, x0[D + i]);
+                }
+                for (int i = 0; i < n; ++i)
+                    if (!std::isfinite(x[i])) return false;
+                samples.push_back(x);
+            }
+            return true;
+        }
+    }
     Vec<R> x = x0, k1, k2, k3, k4, t;
     t.n = n;
     for (int s = 0; s < S; ++s) {

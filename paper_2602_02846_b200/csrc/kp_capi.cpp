@@ -34,6 +34,8 @@ cudaError_t read_check_code(unsigned int* code);
 cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_prop, int grid_sel, cudaStream_t st,
                              int which);
 cudaError_t set_propagate_smem(const KpProblem& P);
+void plan_propagate_smem(KpProblem& P);
+void set_flat_limit(KpProblem& P, int grid_prop);
 
 int propagate_occupancy(const KpProblem& P);
 cudaError_t launch_reset(const KpProblem& P, const KpBuffers& B, unsigned long long seed, cudaStream_t st);
@@ -641,13 +643,18 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         void* hc = nullptr;
         cuda_check(cudaHostAlloc(&hc, sizeof(KpCtl), cudaHostAllocDefault), "cudaHostAlloc ctl");
         pl->h_ctl = static_cast<KpCtl*>(hc);
+        kp::plan_propagate_smem(pl->P);
         cuda_check(kp::set_propagate_smem(P), "smem attribute");
         const int occ = std::max(1, kp::propagate_occupancy(P));
+        if (std::getenv("KP_VERBOSE"))
+            std::fprintf(stderr, "k_propagate: %u B shared (environment %u B, sample-parallel %d: %u items, %u samples), %d blocks/SM\n",
+                         P.prop_smem, P.env_bytes, P.flat_on, P.flat_nb, P.flat_ucap, occ);
         // test hook: KP_PROP_GRID caps the propagate grid, so the multi-group
         // (lane refill) path runs at small item counts
         pl->grid_prop = pl->sms * occ;
         if (const char* g = std::getenv("KP_PROP_GRID")) pl->grid_prop = std::max(1, std::min(pl->grid_prop, std::atoi(g)));
         pl->grid_sel = pl->sms * (1024 / KP_SELECT_THREADS);
+        kp::set_flat_limit(pl->P, pl->grid_prop);
         B.prop_scratch = pl->dalloc<float>(static_cast<size_t>(pl->grid_prop) * (P.n + 1) * 1024);
 
         for (auto*& e : pl->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
@@ -945,6 +952,7 @@ int kp_batch_create(const kp_problem_desc* problem, const kp_config_desc* config
                 cuda_check(cudaSetDevice(pl->device), "cudaSetDevice");
                 pl->grid_prop = std::max(std::max(1, pl->sms / 2), pl->grid_prop * 4 / lanes);
                 pl->grid_sel = std::max(std::max(1, pl->sms / 2), pl->grid_sel * 4 / lanes);
+                kp::set_flat_limit(pl->P, pl->grid_prop);
                 if (pl->graph) cudaGraphExecDestroy(pl->graph);
                 pl->graph = nullptr;
                 capture_graph(pl);

@@ -31,6 +31,7 @@
 // "last block" ticket pattern (threadfence + atomic counter), never a spin.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cmath>
 #include <cstdlib>
 
 #include "kp_math.cuh"
@@ -79,7 +80,7 @@ struct PropCfg {
     // pass of 8 steps cuts its warp-steps by ~22 % (scripts/split_sim.py); for
     // the 4D/6D models the split measured slower (profiles/README.md).
 #ifdef KP_SPLIT_Q
-    static constexpr int SPLIT = MODEL == 3 ? KP_SPLIT_Q : KP_SPLIT_D;
+    static constexpr int SPLIT = MODEL == 3 ? KP_SPLIT_Q : (closed_form<MODEL>() ? 0 : KP_SPLIT_D);
 #else
     static constexpr int SPLIT = MODEL == 3 ? 8 : 0;
 #endif
@@ -103,6 +104,36 @@ struct PropSmem {
     uint32_t chunk;
     unsigned long long cnt[6];
 };
+
+// Work counters of a propagate launch: warp-aggregated, then block-aggregated,
+// then one atomic per counter and block.
+KP_DEV void count_flush(KpCtl* ctl, uint32_t* c, unsigned long long* cnt, int lane) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) c[k] += __shfl_down_sync(0xFFFFFFFFu, c[k], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (c[k]) atomicAdd(&cnt[k], static_cast<unsigned long long>(c[k]));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (cnt[0]) {
+            atomicAdd(&ctl->stats.valid, cnt[0]);
+            atomicAdd(&ctl->n_valid_iter, static_cast<uint32_t>(cnt[0]));
+        }
+        if (cnt[1]) {
+            atomicAdd(&ctl->stats.admitted, cnt[1]);
+            atomicAdd(&ctl->n_adm_iter, static_cast<uint32_t>(cnt[1]));
+        }
+        if (cnt[2]) atomicAdd(&ctl->stats.rk4_steps, cnt[2]);
+        if (cnt[3]) atomicAdd(&ctl->stats.interp_points, cnt[3]);
+        if (cnt[4]) atomicAdd(&ctl->stats.box_tests, cnt[4]);
+        if (cnt[5]) atomicAdd(&ctl->stats.sphere_tests, cnt[5]);
+    }
+}
 
 template <int MODEL>
 KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MODEL>& sh, const Env& E) {
@@ -317,41 +348,256 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
         if (threadIdx.x == 0) sh.chunk = gridDim.x + atomicAdd(&ctl->prop_cursor, 1u);
         __syncthreads();
     }
-    // warp-aggregated then block-aggregated counters
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) c[k] += __shfl_down_sync(0xFFFFFFFFu, c[k], off);
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < 6; ++k)
-            if (c[k]) atomicAdd(&sh.cnt[k], static_cast<unsigned long long>(c[k]));
-    }
+    count_flush(ctl, c, sh.cnt, lane);
+}
+
+// Sample-parallel propagate for the double integrator (closed form, §4 of
+// DESIGN.md).  Its samples do not depend on one another, so a batch of up to
+// flat_nb work items is flattened into its samples and every thread of the
+// block checks a contiguous run of them: the batch takes about
+// (sum of step counts) / threads rounds instead of the longest item's step
+// count, which bounds a one-wave launch in the step-sorted path.  Per batch:
+// (1) one item per thread draws (u, dt), stages the parent state and counts
+// its samples; (2) block scan of the counts; (3) sample checks (bounds,
+// obstacles, interpolated points, segment length into dd[]); an item with a
+// failed sample is flagged and its remaining samples skipped; (4) the owner
+// thread sums its segment lengths in sample order (the sequential recipe's
+// order, so the cost is bit-identical) and admits the candidate.
+template <int MODEL>
+KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, unsigned char* dyn) {
+    constexpr int N = Model<MODEL>::N;
+    constexpr int M = Model<MODEL>::M;
+    constexpr uint32_t T = PropCfg<MODEL>::T;
+    constexpr uint32_t NWARP = T / 32;
+    constexpr int RW = (N + M + 2 + 3) / 4;  // float4 words per item record: x0, u, dt, S
+    constexpr bool TWO_D = (MODEL == 0);
+    __shared__ unsigned long long fcnt[6];
+    __shared__ uint32_t wsum[NWARP];
+    __shared__ uint32_t fchunk;
+    float4* const rec = reinterpret_cast<float4*>(dyn + P.flat_rec);
+    uint32_t* const off = reinterpret_cast<uint32_t*>(dyn + P.flat_offs);           // [T + 1]
+    volatile uint32_t* const bad = reinterpret_cast<uint32_t*>(dyn + P.flat_bad);   // [T]
+    float* const dd = reinterpret_cast<float*>(dyn + P.flat_dd);                    // [flat_ucap]
+    KpCtl* ctl = B.ctl;
+    const uint32_t done = ctl->done, n_items = ctl->n_items, it = ctl->iter;
+    const unsigned long long seed = ctl->seed;
+    if (done) return;
+    if (threadIdx.x < 6) fcnt[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
+    const uint32_t FB = P.flat_nb;  // items per batch (T, or T / 2 for long rollouts)
+    const uint32_t CH = min(T * PropCfg<MODEL>::MAXG, ((n_items + gridDim.x - 1) / gridDim.x + 31u) & ~31u);
+    const uint32_t n_chunks = (n_items + CH - 1) / CH;
+    if (blockIdx.x >= n_chunks) return;
+    const uint32_t* va = B.va[it & 1];
+    const uint32_t cap = P.capacity, S_cap = P.max_slots;
+    const uint32_t lam = static_cast<uint32_t>(P.lambda);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t c[6] = {0, 0, 0, 0, 0, 0};  // valid, admitted, samples, interp, box tests, sphere tests
+    if (threadIdx.x == 0) fchunk = blockIdx.x;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        if (sh.cnt[0]) {
-            atomicAdd(&ctl->stats.valid, sh.cnt[0]);
-            atomicAdd(&ctl->n_valid_iter, static_cast<uint32_t>(sh.cnt[0]));
+    for (;;) {
+        const uint32_t chunk = fchunk;
+        if (chunk >= n_chunks) break;
+        const uint32_t cend = min(chunk * CH + CH, n_items);
+        for (uint32_t b0 = chunk * CH; b0 < cend; b0 += FB) {
+            // (1) one item per thread: draw (u, dt), stage the parent state
+            const uint32_t i = b0 + threadIdx.x;
+            const bool have = threadIdx.x < FB && i < cend;
+            uint32_t node = 0, seff = 0;
+            float acc_p = 0.0f;
+            if (have) {
+                const uint32_t f = i / lam;
+                const uint32_t br = i - f * lam;
+                KP_ASSERT(f < ctl->n_va, 10);
+                node = va[f];
+                KP_ASSERT(node < ctl->n_nodes, 11);
+                float r[RW * 4];
+#pragma unroll
+                for (int w = 0; w < RW * 4; ++w) r[w] = 0.0f;
+#pragma unroll
+                for (int d = 0; d < N; ++d) r[d] = B.state[static_cast<size_t>(d) * cap + node];
+                acc_p = __uint_as_float(B.acc[node]);
+                float u[M], dt;
+                sample_item<M>(P, seed, it, node, br, u, dt);
+                const int S = step_count(P, dt);
+                // the shortened last step may be empty (dt - (S-1) h <= 0): then
+                // the rollout ends at sample S - 1 (as integrate_steps)
+                seff = static_cast<uint32_t>((S > 1 && !(dt - static_cast<float>(S - 1) * P.h > 0.0f)) ? S - 1 : S);
+#pragma unroll
+                for (int d = 0; d < M; ++d) r[N + d] = u[d];
+                r[N + M] = dt;
+                r[N + M + 1] = __int_as_float(S);
+#pragma unroll
+                for (int w = 0; w < RW; ++w)
+                    rec[threadIdx.x * RW + w] = make_float4(r[4 * w], r[4 * w + 1], r[4 * w + 2], r[4 * w + 3]);
+            }
+            bad[threadIdx.x] = 0u;
+            // (2) exclusive scan of the sample counts over the block
+            uint32_t x = seff;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            __syncthreads();
+            if (warp == 0) {
+                uint32_t w = lane < static_cast<int>(NWARP) ? wsum[lane] : 0u;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+                    if (lane >= o) w += y;
+                }
+                if (lane < static_cast<int>(NWARP)) wsum[lane] = w;
+            }
+            __syncthreads();
+            const uint32_t excl = x - seff + (warp ? wsum[warp - 1] : 0u);
+            off[threadIdx.x] = excl;
+            if (threadIdx.x == T - 1) off[T] = excl + seff;
+            __syncthreads();
+            // (3) a contiguous run of samples per thread
+            const uint32_t U = off[T];
+            KP_ASSERT(U <= P.flat_ucap, 14);
+            const uint32_t qa = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x) * U) / T);
+            const uint32_t qb = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x + 1) * U) / T);
+            if (qa < qb) {
+                uint32_t lo = 0, hi = T;  // off[lo] <= qa < off[hi]
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (off[mid] <= qa) lo = mid;
+                    else hi = mid;
+                }
+                uint32_t pi = lo, pbeg = off[lo], pend = off[lo + 1];
+                float x0[N], u[M], dt = 0.0f;
+                int S = 0, prev_s = -1;
+                float ppx = 0.0f, ppy = 0.0f, ppz = 0.0f;
+                bool load = true;
+                for (uint32_t q = qa; q < qb; ++q) {
+                    while (q >= pend) {
+                        ++pi;
+                        pbeg = pend;
+                        pend = off[pi + 1];
+                        load = true;
+                    }
+                    if (load) {
+                        float r[RW * 4];
+#pragma unroll
+                        for (int w = 0; w < RW; ++w) {
+                            const float4 v = rec[pi * RW + w];
+                            r[4 * w] = v.x; r[4 * w + 1] = v.y; r[4 * w + 2] = v.z; r[4 * w + 3] = v.w;
+                        }
+#pragma unroll
+                        for (int d = 0; d < N; ++d) x0[d] = r[d];
+#pragma unroll
+                        for (int d = 0; d < M; ++d) u[d] = r[N + d];
+                        dt = r[N + M];
+                        S = __float_as_int(r[N + M + 1]);
+                        prev_s = -1;
+                        load = false;
+                    }
+                    const int s = static_cast<int>(q - pbeg) + 1;  // sample index 1..seff
+                    float d = 0.0f;
+                    if (!bad[pi]) {
+                        float xs[N];
+                        di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
+                        float px, py, pz;
+                        if (s == 1) {
+                            px = x0[0]; py = x0[1]; pz = TWO_D ? 0.0f : x0[2];
+                        } else if (prev_s == s - 1) {
+                            px = ppx; py = ppy; pz = ppz;
+                        } else {
+                            float xp[N];
+                            di_sample<MODEL>(x0, u, static_cast<float>(s - 1) * P.h, xp);
+                            px = xp[0]; py = xp[1]; pz = TWO_D ? 0.0f : xp[2];
+                        }
+                        ++c[2];
+                        bool ok = true;
+                        if (P.check_finite) {
+#pragma unroll
+                            for (int k = 0; k < N; ++k) ok = ok && isfinite(xs[k]);
+                        }
+                        const float nx = xs[0], ny = xs[1], nz = TWO_D ? 0.0f : xs[2];
+                        const bool inb = within_bounds<MODEL>(P, xs);
+                        const bool hit = in_obstacle(P, E, nx, ny, nz, c[4], c[5]);
+                        ok = ok && inb && !hit;
+                        const float dx = nx - px, dy = ny - py, dz = nz - pz;
+                        float d2 = dx * dx;
+                        d2 = fmaf(dy, dy, d2);
+                        if (!TWO_D) d2 = fmaf(dz, dz, d2);
+                        d = sqrtf(d2);
+                        if (ok && d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, c[3], c[4], c[5]))
+                            ok = false;
+                        if (!ok) bad[pi] = 1u;
+                        ppx = nx; ppy = ny; ppz = nz;
+                        prev_s = s;
+                    }
+                    dd[q] = d;
+                }
+            }
+            __syncthreads();
+            // (4) owner thread: path length in sample order, region, admission
+            if (have && !bad[threadIdx.x]) {
+                float r[RW * 4];
+#pragma unroll
+                for (int w = 0; w < RW; ++w) {
+                    const float4 v = rec[threadIdx.x * RW + w];
+                    r[4 * w] = v.x; r[4 * w + 1] = v.y; r[4 * w + 2] = v.z; r[4 * w + 3] = v.w;
+                }
+                float x0[N], u[M], xs[N];
+#pragma unroll
+                for (int d = 0; d < N; ++d) x0[d] = r[d];
+#pragma unroll
+                for (int d = 0; d < M; ++d) u[d] = r[N + d];
+                const float dt = r[N + M];
+                const int S = __float_as_int(r[N + M + 1]);
+                di_sample<MODEL>(x0, u, (static_cast<int>(seff) == S) ? dt : static_cast<float>(seff) * P.h, xs);
+                const uint32_t q0 = off[threadIdx.x];
+                float total = 0.0f;
+                for (uint32_t k = 0; k < seff; ++k) total += dd[q0 + k];
+                ItemOut o;
+                finish_item<MODEL>(P, xs, dt, total, acc_p, o);
+                ++c[0];
+                const uint32_t bits = __float_as_uint(o.acc);
+                KP_ASSERT(o.region < P.n_regions, 12);
+                KP_ASSERT(i < S_cap, 13);
+                const uint32_t old = atomicMin(B.rc + o.region, bits);
+                if (bits <= old) {  // Improved / Equal admitted, Worse discarded
+                    ++c[1];
+#pragma unroll
+                    for (int d = 0; d < N; ++d) B.vu_state[static_cast<size_t>(d) * S_cap + i] = xs[d];
+#pragma unroll
+                    for (int d = 0; d < M; ++d) B.vu_ctrl[static_cast<size_t>(d) * S_cap + i] = u[d];
+                    B.vu_dt[i] = dt;
+                    B.vu_acc[i] = bits;
+                    B.vu_region[i] = o.region;
+                    atomicOr(B.admit_mask + (i >> 5), 1u << (i & 31));
+                    if (o.goal) atomicOr(B.goal_mask + (i >> 5), 1u << (i & 31));
+                }
+            }
+            __syncthreads();  // the next batch reuses the shared arrays
         }
-        if (sh.cnt[1]) {
-            atomicAdd(&ctl->stats.admitted, sh.cnt[1]);
-            atomicAdd(&ctl->n_adm_iter, static_cast<uint32_t>(sh.cnt[1]));
-        }
-        if (sh.cnt[2]) atomicAdd(&ctl->stats.rk4_steps, sh.cnt[2]);
-        if (sh.cnt[3]) atomicAdd(&ctl->stats.interp_points, sh.cnt[3]);
-        if (sh.cnt[4]) atomicAdd(&ctl->stats.box_tests, sh.cnt[4]);
-        if (sh.cnt[5]) atomicAdd(&ctl->stats.sphere_tests, sh.cnt[5]);
+        if (n_chunks <= gridDim.x) break;  // every chunk was assigned statically
+        if (threadIdx.x == 0) fchunk = gridDim.x + atomicAdd(&ctl->prop_cursor, 1u);
+        __syncthreads();
     }
+    count_flush(ctl, c, fcnt, lane);
 }
 
 template <int MODEL>
 __global__ void __launch_bounds__(PropCfg<MODEL>::T, PropCfg<MODEL>::MIN_BLOCKS) k_propagate(KpProblem P, KpBuffers B) {
-    __shared__ PropSmem<MODEL> sh;
     const Env E = stage_env(P, B);  // constant data: overlaps the predecessor's tail
     pdl_wait();
     pdl_trigger();
-    propagate_phase<MODEL>(P, B, sh, E);
+    unsigned char* const dyn = reinterpret_cast<unsigned char*>(kp_env_smem);
+    if constexpr (closed_form<MODEL>()) {
+        // small launches are latency-bound: flatten them into samples; large
+        // ones are issue-bound, where the step-sorted path runs fewer instructions
+        if (P.flat_on && B.ctl->n_items <= P.flat_max) {
+            flat_phase<MODEL>(P, B, E, dyn);
+            return;
+        }
+    }
+    propagate_phase<MODEL>(P, B, *reinterpret_cast<PropSmem<MODEL>*>(dyn + P.seq_base), E);
 }
 
 // Block-wide inclusive sum of three counters (blockDim == KP_SELECT_THREADS).
@@ -1042,11 +1288,11 @@ __global__ void k_reintegrate(KpProblem P, KpBuffers B, const int32_t* chain, ui
     if (S < 1) S = 1;
     float total = 0.0f;
     float px = x[0], py = x[1], pz = N >= 3 && MODEL != 0 ? x[2] : 0.0f;
+    float x0[N];
+    for (int d = 0; d < N; ++d) x0[d] = x[d];
     uint32_t w = off[j];
     for (int s = 0; s < S; ++s) {
-        const float hk = (s + 1 < S) ? P.h : dt - static_cast<float>(S - 1) * P.h;
-        if (!(hk > 0.0f)) break;
-        rk4_step<MODEL>(P, x, u, hk);
+        if (advance<MODEL>(P, x0, x, u, dt, S, s, P.h / 6.0f) == 1) break;
         for (int d = 0; d < N; ++d) out[static_cast<size_t>(w) * N + d] = x[d];
         ++w;
         const float nx = x[0], ny = x[1], nz = MODEL != 0 ? x[2] : 0.0f;
@@ -1067,7 +1313,65 @@ __global__ void k_reintegrate(KpProblem P, KpBuffers B, const int32_t* chain, ui
 // ------------------------------------------------------------------------
 namespace kp {
 
-size_t propagate_smem(const KpProblem& P) { return P.env_bytes; }
+size_t propagate_smem(const KpProblem& P) { return P.prop_smem; }
+
+// Shared-memory layout of k_propagate after the environment blob: the
+// step-sorted path's PropSmem and (double integrator) the sample-parallel
+// path's arrays share one area.  A sample-parallel batch holds KP_FLAT_ITEMS
+// items and their segment lengths (at most ceil(t_prop / h) + 1 samples each),
+// which keeps the area at the step-sorted path's size: a larger reservation
+// would keep the next kernel's blocks from becoming resident early (PDL).
+// KP_FLAT=0 turns the sample-parallel path off.
+#ifndef KP_FLAT_ITEMS
+#define KP_FLAT_ITEMS 128u
+#endif
+void plan_propagate_smem(KpProblem& P) {
+    auto pad16 = [](size_t b) { return (b + 15) & ~static_cast<size_t>(15); };
+    size_t seq = 0;
+    uint32_t T = 0;
+    switch (P.model) {
+        case 0: seq = sizeof(PropSmem<0>); T = PropCfg<0>::T; break;
+        case 1: seq = sizeof(PropSmem<1>); T = PropCfg<1>::T; break;
+        case 2: seq = sizeof(PropSmem<2>); T = PropCfg<2>::T; break;
+        default: seq = sizeof(PropSmem<3>); T = PropCfg<3>::T; break;
+    }
+    const size_t base = pad16(P.env_bytes);
+    P.seq_base = static_cast<uint32_t>(base);
+    size_t area = pad16(seq);
+    P.flat_on = 0;
+    P.flat_max = 0;
+    const char* env = std::getenv("KP_FLAT");
+    if ((P.model == 0 || P.model == 1) && !(env && env[0] == '0')) {
+        const uint32_t nb = KP_FLAT_ITEMS;
+        const uint32_t rw = static_cast<uint32_t>((P.n + P.m + 2 + 3) / 4);
+        const uint32_t smax = static_cast<uint32_t>(std::ceil(static_cast<double>(P.t_prop) / P.h)) + 1u;
+        const size_t rec = pad16(static_cast<size_t>(nb) * rw * 16);
+        const size_t offs = pad16((T + 1) * 4ull), badb = pad16(T * 4ull);
+        const size_t ucap = static_cast<size_t>(nb) * smax;
+        const size_t flat = rec + offs + badb + pad16(ucap * 4);
+        if (base + flat <= 96 * 1024) {
+            P.flat_on = 1;
+            P.flat_nb = nb;
+            P.flat_rec = static_cast<uint32_t>(base);
+            P.flat_offs = static_cast<uint32_t>(base + rec);
+            P.flat_bad = static_cast<uint32_t>(base + rec + offs);
+            P.flat_dd = static_cast<uint32_t>(base + rec + offs + badb);
+            P.flat_ucap = static_cast<uint32_t>(ucap);
+            area = std::max(area, flat);
+        }
+    }
+    P.prop_smem = static_cast<uint32_t>(base + area);
+}
+
+// Largest launch on the sample-parallel path: one batch per block of the
+// propagate grid (small launches are latency-bound; large ones issue-bound,
+// where the step-sorted path runs fewer instructions).  KP_FLAT_MAX overrides.
+void set_flat_limit(KpProblem& P, int grid_prop) {
+    if (!P.flat_on) return;
+    const char* fm = std::getenv("KP_FLAT_MAX");
+    P.flat_max = fm ? static_cast<uint32_t>(std::strtoul(fm, nullptr, 10))
+                    : P.flat_nb * static_cast<uint32_t>(grid_prop);
+}
 
 static bool pdl_enabled() {
     static const bool on = [] {
@@ -1158,7 +1462,7 @@ cudaError_t launch_debug_propagate(const KpProblem& P, const KpBuffers& B, uint3
                                    const float* pacc, const uint32_t* ids, const uint32_t* brs, uint32_t it,
                                    uint8_t* valid, float* xs, float* us, float* dts, float* accs, uint32_t* regs,
                                    uint32_t* steps, uint8_t* goals, cudaStream_t st) {
-    const size_t smem = propagate_smem(P);
+    const size_t smem = P.env_bytes;  // the environment only (sequential per-item path)
     const int grid = static_cast<int>((n + 127) / 128);
     if (n == 0) return cudaSuccess;
     switch (P.model) {

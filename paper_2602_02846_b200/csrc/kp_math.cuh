@@ -224,6 +224,26 @@ KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk) {
     return rk4_step<MODEL>(P, x, u, hk, hk / 6.0f);
 }
 
+// Double integrator in closed form: RK4 with constant control is exact on it
+// (SPEC.md:138-139), so the sample at time t is evaluated directly,
+// p(t) = p0 + v0 t + (u/2) t^2, v(t) = v0 + u t, with the fused recipe below
+// (DESIGN.md §4).  Every sample depends only on the parent state, not on the
+// previous sample: no rounding accumulates along the segment and the samples of
+// one rollout can be evaluated in any order or in parallel.
+template <int MODEL>
+KP_DEV void di_sample(const float* x0, const float* u, float t, float* x) {
+    constexpr int D = Model<MODEL>::N / 2;  // position dims, then the matching velocities
+    const float tt = t * t;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        x[i] = fmaf(0.5f * u[i], tt, fmaf(x0[D + i], t, x0[i]));
+        x[D + i] = fmaf(u[i], t, x0[D + i]);
+    }
+}
+
+template <int MODEL>
+__host__ __device__ constexpr bool closed_form() { return MODEL == 0 || MODEL == 1; }
+
 // Number of RK4 steps of a segment: samples at 0, h, ..., dt.
 KP_DEV int step_count(const KpProblem& P, float dt) {
     const int S = static_cast<int>(ceilf(dt / P.h));
@@ -399,21 +419,77 @@ struct ItemOut {
 // the path length so far.  Returns 0 (no violation up to s1), 1 invalid,
 // 2 diverged.  The parent (samples[0]) is not re-checked: it is a stored valid
 // node.  Splitting [0, S) at any step is bit-identical to one call.
+// Interpolated points between consecutive samples p and p + (dx, dy, dz),
+// d = ||(dx, dy, dz)|| > collision_step: dyadic subdivision,
+// k = the smallest power of two with d / k <= collision_step (nested points,
+// SPEC.md:231).  d / k and j / k are exact, so multiplying by the exact
+// power-of-two reciprocal equals the division bit-for-bit.  True when a point
+// is inside an obstacle.
+template <bool TWO_D>
+KP_DEV bool segment_hit(const KpProblem& P, const Env& E, float px, float py, float pz, float dx, float dy, float dz,
+                        float d, uint32_t& interp, uint32_t& nbox, uint32_t& nsph) {
+    int k = 2;
+    float rk = 0.5f;
+    while (d * rk > P.coll && k < (1 << 24)) {
+        k <<= 1;
+        rk *= 0.5f;
+    }
+    for (int j = 1; j < k; ++j) {
+        const float t = static_cast<float>(j) * rk;
+        interp += 1;
+        if (in_obstacle(P, E, fmaf(t, dx, px), fmaf(t, dy, py), TWO_D ? 0.0f : fmaf(t, dz, pz), nbox, nsph))
+            return true;
+    }
+    return false;
+}
+
+// Sample s + 1 of a rollout with S steps: the closed form
+// from the parent state x0 for the double integrator, otherwise one RK4 step
+// of x (h6 = h / 6).  Returns 0, 1 when the shortened last step is empty
+// (dt - (S-1) h <= 0: the rollout ends at sample S - 1), 2 when diverged.
+template <int MODEL>
+KP_DEV int advance(const KpProblem& P, const float* x0, float* x, const float* u, float dt, int S, int s, float h6) {
+    if constexpr (closed_form<MODEL>()) {
+        float t = static_cast<float>(s + 1) * P.h;
+        if (s + 1 == S) {
+            const float hk = dt - static_cast<float>(S - 1) * P.h;
+            if (!(hk > 0.0f)) return 1;
+            t = dt;
+        }
+        di_sample<MODEL>(x0, u, t, x);
+        if (P.check_finite) {
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < Model<MODEL>::N; ++i) ok = ok && isfinite(x[i]);
+            if (!ok) return 2;
+        }
+        return 0;
+    } else {
+        float hk = P.h, sixth = h6;
+        if (s + 1 == S) {  // the shortened last step (SPEC.md:135): only here the IEEE division
+            hk = dt - static_cast<float>(S - 1) * P.h;
+            if (!(hk > 0.0f)) return 1;
+            // IEEE div.rn (== hk / 6.0f); volatile so it is not if-converted into every step
+            asm volatile("div.rn.f32 %0, %1, %2;" : "=f"(sixth) : "f"(hk), "f"(6.0f));
+        }
+        return rk4_step<MODEL>(P, x, u, hk, sixth) ? 0 : 2;
+    }
+}
+
 template <int MODEL>
 KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const float* u, float dt, int S, int s0, int s1,
                            float& total, ItemOut& o) {
     constexpr bool TWO_D = (MODEL == 0);
+    constexpr int N = Model<MODEL>::N;
     float px = x[0], py = x[1], pz = TWO_D ? 0.0f : x[2];
     const float h6 = P.h / 6.0f;
+    float x0[N];  // the parent state (closed form: every sample from it; s0 must be 0)
+#pragma unroll
+    for (int i = 0; i < N; ++i) x0[i] = x[i];
     for (int s = s0; s < s1; ++s) {
-        float hk = P.h, sixth = h6;
-        if (s + 1 == S) {  // the shortened last step (SPEC.md:135): only here the IEEE division
-            hk = dt - static_cast<float>(S - 1) * P.h;
-            if (!(hk > 0.0f)) break;
-            // IEEE div.rn (== hk / 6.0f); volatile so it is not if-converted into every step
-            asm volatile("div.rn.f32 %0, %1, %2;" : "=f"(sixth) : "f"(hk), "f"(6.0f));
-        }
-        if (!rk4_step<MODEL>(P, x, u, hk, sixth)) return 2;
+        const int st = advance<MODEL>(P, x0, x, u, dt, S, s, h6);
+        if (st == 1) break;
+        if (st == 2) return 2;
         o.steps += 1;
         const float nx = x[0], ny = x[1], nz = TWO_D ? 0.0f : x[2];
         // bounds and obstacle test without a branch in between (one exit per step;
@@ -426,23 +502,8 @@ KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const flo
         d2 = fmaf(dy, dy, d2);
         if (!TWO_D) d2 = fmaf(dz, dz, d2);
         const float d = sqrtf(d2);
-        if (d2 > P.coll_d2) {  // == (d > P.coll); dyadic subdivision (nested points)
-            // k = 2^e: d / k and j / k are exact, so multiplying by the exact
-            // power-of-two reciprocal equals the division bit-for-bit
-            int k = 2;
-            float rk = 0.5f;
-            while (d * rk > P.coll && k < (1 << 24)) {
-                k <<= 1;
-                rk *= 0.5f;
-            }
-            for (int j = 1; j < k; ++j) {
-                const float t = static_cast<float>(j) * rk;
-                o.interp += 1;
-                if (in_obstacle(P, E, fmaf(t, dx, px), fmaf(t, dy, py), TWO_D ? 0.0f : fmaf(t, dz, pz), o.nbox,
-                                o.nsph))
-                    return 1;
-            }
-        }
+        if (d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, o.interp, o.nbox, o.nsph))
+            return 1;
         total += d;  // cost.hpp:59-61 (position head == workspace dims for every built-in model)
         px = nx; py = ny; pz = nz;
     }

@@ -80,6 +80,15 @@ struct KpProblem {
     int32_t n_cells, n_entries;
     uint32_t env_bytes;        // multiple of 16
     uint32_t off_cells, off_cids;  // byte offsets inside the blob
+    // propagate's shared-memory arrays follow the blob (byte offsets from its start)
+    uint32_t prop_smem;        // total dynamic shared memory of k_propagate
+    uint32_t seq_base;         // step-sorted path: PropSmem<MODEL>
+    // sample-parallel path (double integrator, kp_kernels.cu flat_phase): item
+    // records, sample offsets, invalid flags, per-sample segment lengths
+    int32_t flat_on;
+    uint32_t flat_max;         // launches of at most this many items take the sample-parallel path
+    uint32_t flat_nb;          // items per batch
+    uint32_t flat_rec, flat_offs, flat_bad, flat_dd, flat_ucap;
 };
 
 struct KpStats {

@@ -218,3 +218,24 @@ def test_whole_run_bit_identical_steady_state(scene, iters):
         o = kpo.Oracle(s, kpo.MIRROR32, seed=13, workers=16)
         ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
         _compare_runs(g, o, rg, ro)
+
+
+@pytest.mark.parametrize("mode", ["sample_parallel", "step_sorted"])
+@pytest.mark.parametrize("scene,iters", [("forest_di6", 24), ("zigzag2d", 40)])
+def test_whole_run_bit_identical_propagate_paths(scene, iters, mode, monkeypatch):
+    """The double integrator's two propagate paths (kp_kernels.cu flat_phase for
+    small launches, the step-sorted path for large ones) each reproduce the
+    restatement on their own: forced for every launch size here."""
+    if mode == "sample_parallel":
+        monkeypatch.setenv("KP_FLAT_MAX", str(1 << 30))
+    else:
+        monkeypatch.setenv("KP_FLAT", "0")
+    s = scenarios.load(scene)
+    with Planner(s, seed=21) as g:
+        rg = g.solve(budget_s=0.0, max_iterations=iters)
+    monkeypatch.delenv("KP_FLAT_MAX", raising=False)
+    monkeypatch.delenv("KP_FLAT", raising=False)
+    o = kpo.Oracle(s, kpo.MIRROR32, seed=21, workers=8)
+    ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
+    for k in ("best_cost", "node_count", "propagations_valid", "nodes_committed", "timeline_len"):
+        assert rg[k] == ro[k], (k, rg[k], ro[k])
