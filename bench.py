@@ -501,13 +501,20 @@ def roofline(scenario, pa, pb):
     t_sel = d["t_select_s"] / n_sel
     sel_gbs = sel_bytes / n_sel / t_sel / 1e9 if t_sel > 0 else 0.0
     t_total = d["t_propagate_s"] + d["t_select_s"] + d["t_scatter_s"]
-    traffic = None  # dram read+write bytes per launch from the committed ncu --set full capture
+    traffic, issue = None, None  # from the committed ncu --set full capture of a steady-state launch
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         cfg_name = scenario.get("name", "")
         mi = {'double_integrator_4d': 0, 'double_integrator_6d': 1, 'dubins_airplane_6d': 2, 'quadcopter_12d': 3}[model]
         ent = tr.get(cfg_name, {})
-        traffic = (ent.get(f"k_propagate<{mi}>") or ent.get(f"kp::k_propagate<{mi}>") or {}).get("dram_bytes")
+        rec = ent.get(f"k_propagate<{mi}>") or ent.get(f"kp::k_propagate<{mi}>") or {}
+        traffic = rec.get("dram_bytes")
+        if rec.get("issue_active_pct") is not None:
+            # the resource the launch is actually bound by: instruction issue
+            # (FP32 is a minority of the issued instructions; SIMT = active lanes / 32)
+            issue = {"issue_active_frac": rec["issue_active_pct"] / 100.0,
+                     "simt_lanes_per_inst": rec.get("simt"), "warp_inst_per_launch": rec.get("warp_inst"),
+                     "fp32_share_of_thread_inst": rec.get("fp32_share"), "source": rec.get("source")}
     except Exception:
         pass
     return {
@@ -516,6 +523,7 @@ def roofline(scenario, pa, pb):
         "achieved": achieved / 1e12, "peak": pk["fp32_lane_ops"] / 1e12, "unit": "T lane-op/s",
         "frac": achieved / pk["fp32_lane_ops"], "traffic": traffic,
         "traffic_note": "dram bytes/launch of a steady-state launch, profiles/ncu_traffic.json (working set is L2-resident)",
+        "issue": issue,
         "peak_src": pk["fp32_src"],
         "ops_per_launch": ops_launch, "avg_launch_us": t_prop * 1e6, "launches": n_prop,
         "ops_convention": "FP32 lane-ops of the pinned recipe: FFMA, FADD, FMUL, FSETP, FMNMX, FDIV each = 1",
