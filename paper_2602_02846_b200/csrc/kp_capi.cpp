@@ -650,7 +650,7 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
             std::fprintf(stderr, "k_propagate: %u B shared (environment %u B, sample-parallel %d: %u items, %u samples), %d blocks/SM\n",
                          P.prop_smem, P.env_bytes, P.flat_on, P.flat_nb, P.flat_ucap, occ);
         // test hook: KP_PROP_GRID caps the propagate grid, so the multi-group
-        // (lane refill) path runs at small item counts
+        // paths (several groups per warp, split rollouts) run at small item counts
         pl->grid_prop = pl->sms * occ;
         if (const char* g = std::getenv("KP_PROP_GRID")) pl->grid_prop = std::max(1, std::min(pl->grid_prop, std::atoi(g)));
         pl->grid_sel = pl->sms * (1024 / KP_SELECT_THREADS);

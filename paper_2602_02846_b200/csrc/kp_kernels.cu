@@ -78,7 +78,9 @@ struct PropCfg {
     // Steps of the first pass of a split rollout (0: never split).  Only the
     // quadcopter splits: ~55 % of its items stop early (invalid), and a first
     // pass of 8 steps cuts its warp-steps by ~22 % (scripts/split_sim.py); for
-    // the 4D/6D models the split measured slower (profiles/README.md).
+    // the 4D/6D models the split measured slower (profiles/README.md), and the
+    // closed-form double integrator cannot resume from a parked state (its
+    // samples derive from the parent state).  -DKP_SPLIT_Q/-DKP_SPLIT_D: A/B builds.
 #ifdef KP_SPLIT_Q
     static constexpr int SPLIT = MODEL == 3 ? KP_SPLIT_Q : (closed_form<MODEL>() ? 0 : KP_SPLIT_D);
 #else
