@@ -905,7 +905,7 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
     const uint32_t it1 = it + 1;
     const unsigned long long best = ctl->best;
     const uint32_t tl_len = ctl->timeline_len;
-    const unsigned long long prev = tl_len ? ctl->timeline[tl_len - 1].best : ~0ull;
+    const unsigned long long prev = ctl->tl_best;  // == tl_len ? timeline[tl_len - 1].best : ~0
     const unsigned long long t_start = ctl->t_start_ns, first_ns = ctl->first_ns, deadline = ctl->deadline_ns;
     const unsigned long long t_prop = ctl->t_prop_ns, t_sel = ctl->t_sel_ns, t_scat = ctl->t_scat_ns;
     const uint32_t max_iter_abs = ctl->max_iter_abs, stop_first = ctl->stop_first;
@@ -933,6 +933,7 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
             t.t_ns = now - t_start;
             t.best = best;
             ctl->timeline_len = tl_len + 1;
+            ctl->tl_best = best;
         }
         if (first_ns == 0) {
             ctl->first_ns = now - t_start;
@@ -1200,6 +1201,7 @@ __global__ void k_reset_root(KpProblem P, KpBuffers B, unsigned long long seed) 
     ctl->n_nodes = 1;
     ctl->n_items = static_cast<uint32_t>(P.lambda);
     ctl->best = ~0ull;
+    ctl->tl_best = ~0ull;
 }
 
 // Start of a kp_solve call: budget, iteration cap, immediate termination test.

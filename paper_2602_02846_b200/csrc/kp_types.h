@@ -138,6 +138,7 @@ struct KpCtl {
     uint32_t first_iter, best_iter;
     unsigned long long seed;  // run seed (kept here so captured graphs survive kp_reset)
     unsigned long long best;  // (cost bits << 32) | leaf ; init ~0
+    unsigned long long tl_best;  // best of the last timeline entry (init ~0): no dependent load at the boundary
     unsigned long long t_start_ns, deadline_ns, t_last_ns;
     unsigned long long first_ns, best_ns;
     unsigned long long t_prop_ns, t_sel_ns, t_sel_end_ns, t_scat_ns;  // current iteration stamps
