@@ -533,6 +533,20 @@ typename P::R segment_cost(const ProblemDef& pd, const Consts<P>& k,
     if (!(duration > 0)) throw InvalidSegmentError("segment_cost: segment duration must be positive");
     if (pd.cost == CostKind::ControlDuration) return duration;
     const int d = pd.cost_position_dims;
+    if constexpr (P::kClosedFormDI) {
+        if (pd.model == ModelId::DI4 || pd.model == ModelId::DI6) {
+            // device recipe: segment lengths rounded to multiples
+            // of 2^-40, summed exactly as a 64-bit integer, one rounding to R
+            long long fx = 0;
+            for (size_t i = 1; i < samples.size(); ++i) {
+                R dl[kMaxStateDim];
+                for (int j = 0; j < d; ++j) dl[j] = samples[i][j] - samples[i - 1][j];
+                fx += std::llrint(static_cast<double>(pos_delta_norm<P>(d, dl)) * 0x1p40);
+            }
+            if (fx == 0) return k.zero_rate * duration;
+            return static_cast<R>(fx) * R(0x1p-40);
+        }
+    }
     R total = 0;
     for (size_t i = 1; i < samples.size(); ++i) {
         R dl[kMaxStateDim];

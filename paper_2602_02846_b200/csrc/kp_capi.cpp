@@ -647,8 +647,8 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         cuda_check(kp::set_propagate_smem(P), "smem attribute");
         const int occ = std::max(1, kp::propagate_occupancy(P));
         if (std::getenv("KP_VERBOSE"))
-            std::fprintf(stderr, "k_propagate: %u B shared (environment %u B, sample-parallel %d: %u items, %u samples), %d blocks/SM\n",
-                         P.prop_smem, P.env_bytes, P.flat_on, P.flat_nb, P.flat_ucap, occ);
+            std::fprintf(stderr, "k_propagate: %u B shared (environment %u B, sample-parallel %d: %u items), %d blocks/SM\n",
+                         P.prop_smem, P.env_bytes, P.flat_on, P.flat_nb, occ);
         // test hook: KP_PROP_GRID caps the propagate grid, so the multi-group
         // paths (several groups per warp, split rollouts) run at small item counts
         pl->grid_prop = pl->sms * occ;

@@ -379,7 +379,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
     float4* const rec = reinterpret_cast<float4*>(dyn + P.flat_rec);
     uint32_t* const off = reinterpret_cast<uint32_t*>(dyn + P.flat_offs);           // [T + 1]
     volatile uint32_t* const bad = reinterpret_cast<uint32_t*>(dyn + P.flat_bad);   // [T]
-    float* const dd = reinterpret_cast<float*>(dyn + P.flat_dd);                    // [flat_ucap]
+    unsigned long long* const len = reinterpret_cast<unsigned long long*>(dyn + P.flat_len);  // [T] fixed point
     KpCtl* ctl = B.ctl;
     const uint32_t done = ctl->done, n_items = ctl->n_items, it = ctl->iter;
     const unsigned long long seed = ctl->seed;
@@ -434,6 +434,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                     rec[threadIdx.x * RW + w] = make_float4(r[4 * w], r[4 * w + 1], r[4 * w + 2], r[4 * w + 3]);
             }
             bad[threadIdx.x] = 0u;
+            len[threadIdx.x] = 0ull;
             // (2) exclusive scan of the sample counts over the block
             uint32_t x = seff;
 #pragma unroll
@@ -459,7 +460,6 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
             __syncthreads();
             // (3) a contiguous run of samples per thread
             const uint32_t U = off[T];
-            KP_ASSERT(U <= P.flat_ucap, 14);
             const uint32_t qa = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x) * U) / T);
             const uint32_t qb = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x + 1) * U) / T);
             if (qa < qb) {
@@ -474,8 +474,11 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 int S = 0, prev_s = -1;
                 float ppx = 0.0f, ppy = 0.0f, ppz = 0.0f;
                 bool load = true;
+                long long run = 0;  // fixed-point length of this thread's run of item pi
                 for (uint32_t q = qa; q < qb; ++q) {
                     while (q >= pend) {
+                        if (run) atomicAdd(len + pi, static_cast<unsigned long long>(run));
+                        run = 0;
                         ++pi;
                         pbeg = pend;
                         pend = off[pi + 1];
@@ -498,7 +501,6 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                         load = false;
                     }
                     const int s = static_cast<int>(q - pbeg) + 1;  // sample index 1..seff
-                    float d = 0.0f;
                     if (!bad[pi]) {
                         float xs[N];
                         di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
@@ -526,15 +528,16 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                         float d2 = dx * dx;
                         d2 = fmaf(dy, dy, d2);
                         if (!TWO_D) d2 = fmaf(dz, dz, d2);
-                        d = sqrtf(d2);
+                        const float d = sqrtf(d2);
                         if (ok && d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, c[3], c[4], c[5]))
                             ok = false;
                         if (!ok) bad[pi] = 1u;
+                        run += len_fixed(d);
                         ppx = nx; ppy = ny; ppz = nz;
                         prev_s = s;
                     }
-                    dd[q] = d;
                 }
+                if (run) atomicAdd(len + pi, static_cast<unsigned long long>(run));
             }
             __syncthreads();
             // (4) owner thread: path length in sample order, region, admission
@@ -553,11 +556,8 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 const float dt = r[N + M];
                 const int S = __float_as_int(r[N + M + 1]);
                 di_sample<MODEL>(x0, u, (static_cast<int>(seff) == S) ? dt : static_cast<float>(seff) * P.h, xs);
-                const uint32_t q0 = off[threadIdx.x];
-                float total = 0.0f;
-                for (uint32_t k = 0; k < seff; ++k) total += dd[q0 + k];
                 ItemOut o;
-                finish_item<MODEL>(P, xs, dt, total, acc_p, o);
+                finish_item<MODEL>(P, xs, dt, fixed_len(static_cast<long long>(len[threadIdx.x])), acc_p, o);
                 ++c[0];
                 const uint32_t bits = __float_as_uint(o.acc);
                 KP_ASSERT(o.region < P.n_regions, 12);
@@ -1291,6 +1291,7 @@ __global__ void k_reintegrate(KpProblem P, KpBuffers B, const int32_t* chain, ui
     int S = static_cast<int>(ceilf(q));
     if (S < 1) S = 1;
     float total = 0.0f;
+    long long fx = 0;
     float px = x[0], py = x[1], pz = N >= 3 && MODEL != 0 ? x[2] : 0.0f;
     float x0[N];
     for (int d = 0; d < N; ++d) x0[d] = x[d];
@@ -1304,9 +1305,11 @@ __global__ void k_reintegrate(KpProblem P, KpBuffers B, const int32_t* chain, ui
         float d2 = dx * dx;
         d2 = fmaf(dy, dy, d2);
         if (MODEL != 0) d2 = fmaf(dz, dz, d2);
-        total += sqrtf(d2);
+        if constexpr (closed_form<MODEL>()) fx += len_fixed(sqrtf(d2));
+        else total += sqrtf(d2);
         px = nx; py = ny; pz = nz;
     }
+    if constexpr (closed_form<MODEL>()) total = fixed_len(fx);
     seg_cost[j] = P.cost_kind == 1 ? dt : (total == 0.0f ? P.zero_rate * dt : total);
 }
 
@@ -1321,13 +1324,13 @@ size_t propagate_smem(const KpProblem& P) { return P.prop_smem; }
 
 // Shared-memory layout of k_propagate after the environment blob: the
 // step-sorted path's PropSmem and (double integrator) the sample-parallel
-// path's arrays share one area.  A sample-parallel batch holds KP_FLAT_ITEMS
-// items and their segment lengths (at most ceil(t_prop / h) + 1 samples each),
-// which keeps the area at the step-sorted path's size: a larger reservation
-// would keep the next kernel's blocks from becoming resident early (PDL).
-// KP_FLAT=0 turns the sample-parallel path off.
+// path's arrays share one area (a larger reservation than the step-sorted
+// path's would keep the next kernel's blocks from becoming resident early
+// under PDL).  A sample-parallel batch holds KP_FLAT_ITEMS item records,
+// sample offsets, invalid flags and fixed-point path lengths.  KP_FLAT=0
+// turns the sample-parallel path off.
 #ifndef KP_FLAT_ITEMS
-#define KP_FLAT_ITEMS 128u
+#define KP_FLAT_ITEMS 512u
 #endif
 void plan_propagate_smem(KpProblem& P) {
     auto pad16 = [](size_t b) { return (b + 15) & ~static_cast<size_t>(15); };
@@ -1346,21 +1349,18 @@ void plan_propagate_smem(KpProblem& P) {
     P.flat_max = 0;
     const char* env = std::getenv("KP_FLAT");
     if ((P.model == 0 || P.model == 1) && !(env && env[0] == '0')) {
-        const uint32_t nb = KP_FLAT_ITEMS;
+        const uint32_t nb = std::min<uint32_t>(KP_FLAT_ITEMS, T);
         const uint32_t rw = static_cast<uint32_t>((P.n + P.m + 2 + 3) / 4);
-        const uint32_t smax = static_cast<uint32_t>(std::ceil(static_cast<double>(P.t_prop) / P.h)) + 1u;
         const size_t rec = pad16(static_cast<size_t>(nb) * rw * 16);
-        const size_t offs = pad16((T + 1) * 4ull), badb = pad16(T * 4ull);
-        const size_t ucap = static_cast<size_t>(nb) * smax;
-        const size_t flat = rec + offs + badb + pad16(ucap * 4);
+        const size_t offs = pad16((T + 1) * 4ull), badb = pad16(T * 4ull), lenb = pad16(T * 8ull);
+        const size_t flat = rec + offs + badb + lenb;
         if (base + flat <= 96 * 1024) {
             P.flat_on = 1;
             P.flat_nb = nb;
             P.flat_rec = static_cast<uint32_t>(base);
             P.flat_offs = static_cast<uint32_t>(base + rec);
             P.flat_bad = static_cast<uint32_t>(base + rec + offs);
-            P.flat_dd = static_cast<uint32_t>(base + rec + offs + badb);
-            P.flat_ucap = static_cast<uint32_t>(ucap);
+            P.flat_len = static_cast<uint32_t>(base + rec + offs + badb);
             area = std::max(area, flat);
         }
     }

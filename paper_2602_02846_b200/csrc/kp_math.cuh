@@ -244,6 +244,14 @@ KP_DEV void di_sample(const float* x0, const float* u, float t, float* x) {
 template <int MODEL>
 __host__ __device__ constexpr bool closed_form() { return MODEL == 0 || MODEL == 1; }
 
+// Path length of a closed-form rollout (DECISION): every segment
+// length is rounded to a multiple of 2^-40 and the multiples are summed as a
+// 64-bit integer, so the sum is exact and independent of the order in which
+// segments are added (the sample-parallel path adds them from several threads);
+// one rounding back to fp32 at the end.  d * 2^40 is exact in fp32.
+KP_DEV long long len_fixed(float d) { return __float2ll_rn(d * 0x1p40f); }
+KP_DEV float fixed_len(long long s) { return __ll2float_rn(s) * 0x1p-40f; }
+
 // Number of RK4 steps of a segment: samples at 0, h, ..., dt.
 KP_DEV int step_count(const KpProblem& P, float dt) {
     const int S = static_cast<int>(ceilf(dt / P.h));
@@ -486,6 +494,7 @@ KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const flo
     float x0[N];  // the parent state (closed form: every sample from it; s0 must be 0)
 #pragma unroll
     for (int i = 0; i < N; ++i) x0[i] = x[i];
+    long long fx = 0;  // closed form: fixed-point path length
     for (int s = s0; s < s1; ++s) {
         const int st = advance<MODEL>(P, x0, x, u, dt, S, s, h6);
         if (st == 1) break;
@@ -504,9 +513,12 @@ KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const flo
         const float d = sqrtf(d2);
         if (d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, o.interp, o.nbox, o.nsph))
             return 1;
-        total += d;  // cost.hpp:59-61 (position head == workspace dims for every built-in model)
+        // cost.hpp:59-61 (position head == workspace dims for every built-in model)
+        if constexpr (closed_form<MODEL>()) fx += len_fixed(d);
+        else total += d;
         px = nx; py = ny; pz = nz;
     }
+    if constexpr (closed_form<MODEL>()) total = fixed_len(fx);
     return 0;
 }
 

@@ -84,11 +84,11 @@ struct KpProblem {
     uint32_t prop_smem;        // total dynamic shared memory of k_propagate
     uint32_t seq_base;         // step-sorted path: PropSmem<MODEL>
     // sample-parallel path (double integrator, kp_kernels.cu flat_phase): item
-    // records, sample offsets, invalid flags, per-sample segment lengths
+    // records, sample offsets, invalid flags, fixed-point path lengths
     int32_t flat_on;
     uint32_t flat_max;         // launches of at most this many items take the sample-parallel path
     uint32_t flat_nb;          // items per batch
-    uint32_t flat_rec, flat_offs, flat_bad, flat_dd, flat_ucap;
+    uint32_t flat_rec, flat_offs, flat_bad, flat_len;
 };
 
 struct KpStats {
