@@ -379,7 +379,10 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
     float4* const rec = reinterpret_cast<float4*>(dyn + P.flat_rec);
     uint32_t* const off = reinterpret_cast<uint32_t*>(dyn + P.flat_offs);           // [T + 1]
     volatile uint32_t* const bad = reinterpret_cast<uint32_t*>(dyn + P.flat_bad);   // [T]
-    unsigned long long* const len = reinterpret_cast<unsigned long long*>(dyn + P.flat_len);  // [T] fixed point
+    // fixed-point path lengths as two 32-bit limbs (native shared atomics):
+    // len = hi << 24 + lo, every run adding its low 24 bits to lo and the rest to hi
+    uint32_t* const len_lo = reinterpret_cast<uint32_t*>(dyn + P.flat_len);  // [T]
+    uint32_t* const len_hi = len_lo + T;                                    // [T]
     KpCtl* ctl = B.ctl;
     const uint32_t done = ctl->done, n_items = ctl->n_items, it = ctl->iter;
     const unsigned long long seed = ctl->seed;
@@ -434,7 +437,8 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                     rec[threadIdx.x * RW + w] = make_float4(r[4 * w], r[4 * w + 1], r[4 * w + 2], r[4 * w + 3]);
             }
             bad[threadIdx.x] = 0u;
-            len[threadIdx.x] = 0ull;
+            len_lo[threadIdx.x] = 0u;
+            len_hi[threadIdx.x] = 0u;
             // (2) exclusive scan of the sample counts over the block
             uint32_t x = seff;
 #pragma unroll
@@ -473,18 +477,25 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 float x0[N], u[M], dt = 0.0f;
                 int S = 0, prev_s = -1;
                 float ppx = 0.0f, ppy = 0.0f, ppz = 0.0f;
-                bool load = true;
                 long long run = 0;  // fixed-point length of this thread's run of item pi
-                for (uint32_t q = qa; q < qb; ++q) {
-                    while (q >= pend) {
-                        if (run) atomicAdd(len + pi, static_cast<unsigned long long>(run));
-                        run = 0;
-                        ++pi;
-                        pbeg = pend;
-                        pend = off[pi + 1];
-                        load = true;
+                auto flush = [&](uint32_t item) {
+                    if (run) {
+                        atomicAdd(len_lo + item, static_cast<uint32_t>(run & 0xFFFFFF));
+                        atomicAdd(len_hi + item, static_cast<uint32_t>(run >> 24));
                     }
-                    if (load) {
+                    run = 0;
+                };
+                for (uint32_t q = qa; q < qb; ++q) {
+                    if (q >= pend) {  // next item with samples (zero-sample items are skipped)
+                        flush(pi);
+                        do {
+                            ++pi;
+                            pbeg = pend;
+                            pend = off[pi + 1];
+                        } while (q >= pend);
+                        prev_s = -1;
+                    }
+                    {  // the item record, every sample: lanes change items at different samples
                         float r[RW * 4];
 #pragma unroll
                         for (int w = 0; w < RW; ++w) {
@@ -497,8 +508,6 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                         for (int d = 0; d < M; ++d) u[d] = r[N + d];
                         dt = r[N + M];
                         S = __float_as_int(r[N + M + 1]);
-                        prev_s = -1;
-                        load = false;
                     }
                     const int s = static_cast<int>(q - pbeg) + 1;  // sample index 1..seff
                     if (!bad[pi]) {
@@ -537,7 +546,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                         prev_s = s;
                     }
                 }
-                if (run) atomicAdd(len + pi, static_cast<unsigned long long>(run));
+                flush(pi);
             }
             __syncthreads();
             // (4) owner thread: path length in sample order, region, admission
@@ -557,7 +566,8 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 const int S = __float_as_int(r[N + M + 1]);
                 di_sample<MODEL>(x0, u, (static_cast<int>(seff) == S) ? dt : static_cast<float>(seff) * P.h, xs);
                 ItemOut o;
-                finish_item<MODEL>(P, xs, dt, fixed_len(static_cast<long long>(len[threadIdx.x])), acc_p, o);
+                const long long fx = (static_cast<long long>(len_hi[threadIdx.x]) << 24) + len_lo[threadIdx.x];
+                finish_item<MODEL>(P, xs, dt, fixed_len(fx), acc_p, o);
                 ++c[0];
                 const uint32_t bits = __float_as_uint(o.acc);
                 KP_ASSERT(o.region < P.n_regions, 12);
@@ -1352,7 +1362,7 @@ void plan_propagate_smem(KpProblem& P) {
         const uint32_t nb = std::min<uint32_t>(KP_FLAT_ITEMS, T);
         const uint32_t rw = static_cast<uint32_t>((P.n + P.m + 2 + 3) / 4);
         const size_t rec = pad16(static_cast<size_t>(nb) * rw * 16);
-        const size_t offs = pad16((T + 1) * 4ull), badb = pad16(T * 4ull), lenb = pad16(T * 8ull);
+        const size_t offs = pad16((T + 1) * 4ull), badb = pad16(T * 4ull), lenb = pad16(2 * T * 4ull);
         const size_t flat = rec + offs + badb + lenb;
         if (base + flat <= 96 * 1024) {
             P.flat_on = 1;
