@@ -365,7 +365,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
 // failed sample is flagged and its remaining samples skipped; (4) the owner
 // thread sums its segment lengths in sample order (the sequential recipe's
 // order, so the cost is bit-identical) and admits the candidate.
-template <int MODEL>
+template <int MODEL, bool IL>
 KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, unsigned char* dyn) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
@@ -462,91 +462,154 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
             off[threadIdx.x] = excl;
             if (threadIdx.x == T - 1) off[T] = excl + seff;
             __syncthreads();
-            // (3) a contiguous run of samples per thread
-            const uint32_t U = off[T];
-            const uint32_t qa = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x) * U) / T);
-            const uint32_t qb = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x + 1) * U) / T);
-            if (qa < qb) {
-                uint32_t lo = 0, hi = T;  // off[lo] <= qa < off[hi]
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (off[mid] <= qa) lo = mid;
-                    else hi = mid;
+            if constexpr (IL) {
+                // (3) samples interleaved over the block: round r, thread t checks
+                // sample r*T + t, so a warp's lanes hold consecutive samples of a
+                // few items (nearby points: coherent broad / narrow phases)
+                const uint32_t U = off[T];
+                uint16_t* const idx = reinterpret_cast<uint16_t*>(dyn + P.flat_idx);  // item of sample 32k
+                if (seff) {
+                    for (uint32_t m = (excl + 31) >> 5; (m << 5) < excl + seff; ++m) idx[m] = static_cast<uint16_t>(threadIdx.x);
                 }
-                uint32_t pi = lo, pbeg = off[lo], pend = off[lo + 1];
-                float x0[N], u[M], dt = 0.0f;
-                int S = 0, prev_s = -1;
-                float ppx = 0.0f, ppy = 0.0f, ppz = 0.0f;
-                long long run = 0;  // fixed-point length of this thread's run of item pi
-                auto flush = [&](uint32_t item) {
-                    if (run) {
-                        atomicAdd(len_lo + item, static_cast<uint32_t>(run & 0xFFFFFF));
-                        atomicAdd(len_hi + item, static_cast<uint32_t>(run >> 24));
-                    }
-                    run = 0;
-                };
-                for (uint32_t q = qa; q < qb; ++q) {
-                    if (q >= pend) {  // next item with samples (zero-sample items are skipped)
-                        flush(pi);
-                        do {
-                            ++pi;
-                            pbeg = pend;
-                            pend = off[pi + 1];
-                        } while (q >= pend);
-                        prev_s = -1;
-                    }
-                    {  // the item record, every sample: lanes change items at different samples
-                        float r[RW * 4];
+                __syncthreads();
+                for (uint32_t q0 = 0; q0 < U; q0 += T) {
+                    const uint32_t q = q0 + threadIdx.x;
+                    if (q >= U) break;
+                    uint32_t pi = idx[q >> 5];
+                    while (off[pi + 1] <= q) ++pi;
+                    if (bad[pi]) continue;
+                    float x0[N], u[M];
+                    float r[RW * 4];
 #pragma unroll
-                        for (int w = 0; w < RW; ++w) {
-                            const float4 v = rec[pi * RW + w];
-                            r[4 * w] = v.x; r[4 * w + 1] = v.y; r[4 * w + 2] = v.z; r[4 * w + 3] = v.w;
-                        }
-#pragma unroll
-                        for (int d = 0; d < N; ++d) x0[d] = r[d];
-#pragma unroll
-                        for (int d = 0; d < M; ++d) u[d] = r[N + d];
-                        dt = r[N + M];
-                        S = __float_as_int(r[N + M + 1]);
+                    for (int w = 0; w < RW; ++w) {
+                        const float4 v = rec[pi * RW + w];
+                        r[4 * w] = v.x; r[4 * w + 1] = v.y; r[4 * w + 2] = v.z; r[4 * w + 3] = v.w;
                     }
-                    const int s = static_cast<int>(q - pbeg) + 1;  // sample index 1..seff
-                    if (!bad[pi]) {
-                        float xs[N];
-                        di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
-                        float px, py, pz;
-                        if (s == 1) {
-                            px = x0[0]; py = x0[1]; pz = TWO_D ? 0.0f : x0[2];
-                        } else if (prev_s == s - 1) {
-                            px = ppx; py = ppy; pz = ppz;
-                        } else {
-                            float xp[N];
-                            di_sample<MODEL>(x0, u, static_cast<float>(s - 1) * P.h, xp);
-                            px = xp[0]; py = xp[1]; pz = TWO_D ? 0.0f : xp[2];
-                        }
-                        ++c[2];
-                        bool ok = true;
-                        if (P.check_finite) {
 #pragma unroll
-                            for (int k = 0; k < N; ++k) ok = ok && isfinite(xs[k]);
-                        }
-                        const float nx = xs[0], ny = xs[1], nz = TWO_D ? 0.0f : xs[2];
-                        const bool inb = within_bounds<MODEL>(P, xs);
-                        const bool hit = in_obstacle(P, E, nx, ny, nz, c[4], c[5]);
-                        ok = ok && inb && !hit;
-                        const float dx = nx - px, dy = ny - py, dz = nz - pz;
-                        float d2 = dx * dx;
-                        d2 = fmaf(dy, dy, d2);
-                        if (!TWO_D) d2 = fmaf(dz, dz, d2);
-                        const float d = sqrtf(d2);
-                        if (ok && d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, c[3], c[4], c[5]))
-                            ok = false;
-                        if (!ok) bad[pi] = 1u;
-                        run += len_fixed(d);
-                        ppx = nx; ppy = ny; ppz = nz;
-                        prev_s = s;
+                    for (int d = 0; d < N; ++d) x0[d] = r[d];
+#pragma unroll
+                    for (int d = 0; d < M; ++d) u[d] = r[N + d];
+                    const float dt = r[N + M];
+                    const int S = __float_as_int(r[N + M + 1]);
+                    const int s = static_cast<int>(q - off[pi]) + 1;
+                    float xs[N], xp[N];
+                    di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
+                    if (s == 1) {
+#pragma unroll
+                        for (int d = 0; d < N; ++d) xp[d] = x0[d];
+                    } else {
+                        di_sample<MODEL>(x0, u, static_cast<float>(s - 1) * P.h, xp);
                     }
+                    const float px = xp[0], py = xp[1], pz = TWO_D ? 0.0f : xp[2];
+                    ++c[2];
+                    bool ok = true;
+                    if (P.check_finite) {
+#pragma unroll
+                        for (int k = 0; k < N; ++k) ok = ok && isfinite(xs[k]);
+                    }
+                    const float nx = xs[0], ny = xs[1], nz = TWO_D ? 0.0f : xs[2];
+                    const bool inb = within_bounds<MODEL>(P, xs);
+                    const bool hit = in_obstacle(P, E, nx, ny, nz, c[4], c[5]);
+                    ok = ok && inb && !hit;
+                    const float dx = nx - px, dy = ny - py, dz = nz - pz;
+                    float d2 = dx * dx;
+                    d2 = fmaf(dy, dy, d2);
+                    if (!TWO_D) d2 = fmaf(dz, dz, d2);
+                    const float d = sqrtf(d2);
+                    if (ok && d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, c[3], c[4], c[5]))
+                        ok = false;
+                    if (!ok) bad[pi] = 1u;
+                    const long long fx = len_fixed(d);
+                    atomicAdd(len_lo + pi, static_cast<uint32_t>(fx & 0xFFFFFF));
+                    atomicAdd(len_hi + pi, static_cast<uint32_t>(fx >> 24));
                 }
-                flush(pi);
+            } else {
+                // (3) a contiguous run of samples per thread
+                const uint32_t U = off[T];
+                const uint32_t qa = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x) * U) / T);
+                const uint32_t qb = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x + 1) * U) / T);
+                if (qa < qb) {
+                    uint32_t lo = 0, hi = T;  // off[lo] <= qa < off[hi]
+                    while (hi - lo > 1) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (off[mid] <= qa) lo = mid;
+                        else hi = mid;
+                    }
+                    uint32_t pi = lo, pbeg = off[lo], pend = off[lo + 1];
+                    float x0[N], u[M], dt = 0.0f;
+                    int S = 0, prev_s = -1;
+                    float ppx = 0.0f, ppy = 0.0f, ppz = 0.0f;
+                    long long run = 0;  // fixed-point length of this thread's run of item pi
+                    auto flush = [&](uint32_t item) {
+                        if (run) {
+                            atomicAdd(len_lo + item, static_cast<uint32_t>(run & 0xFFFFFF));
+                            atomicAdd(len_hi + item, static_cast<uint32_t>(run >> 24));
+                        }
+                        run = 0;
+                    };
+                    for (uint32_t q = qa; q < qb; ++q) {
+                        if (q >= pend) {  // next item with samples (zero-sample items are skipped)
+                            flush(pi);
+                            do {
+                                ++pi;
+                                pbeg = pend;
+                                pend = off[pi + 1];
+                            } while (q >= pend);
+                            prev_s = -1;
+                        }
+                        {  // the item record, every sample: lanes change items at different samples
+                            float r[RW * 4];
+#pragma unroll
+                            for (int w = 0; w < RW; ++w) {
+                                const float4 v = rec[pi * RW + w];
+                                r[4 * w] = v.x; r[4 * w + 1] = v.y; r[4 * w + 2] = v.z; r[4 * w + 3] = v.w;
+                            }
+#pragma unroll
+                            for (int d = 0; d < N; ++d) x0[d] = r[d];
+#pragma unroll
+                            for (int d = 0; d < M; ++d) u[d] = r[N + d];
+                            dt = r[N + M];
+                            S = __float_as_int(r[N + M + 1]);
+                        }
+                        const int s = static_cast<int>(q - pbeg) + 1;  // sample index 1..seff
+                        if (!bad[pi]) {
+                            float xs[N];
+                            di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
+                            float px, py, pz;
+                            if (s == 1) {
+                                px = x0[0]; py = x0[1]; pz = TWO_D ? 0.0f : x0[2];
+                            } else if (prev_s == s - 1) {
+                                px = ppx; py = ppy; pz = ppz;
+                            } else {
+                                float xp[N];
+                                di_sample<MODEL>(x0, u, static_cast<float>(s - 1) * P.h, xp);
+                                px = xp[0]; py = xp[1]; pz = TWO_D ? 0.0f : xp[2];
+                            }
+                            ++c[2];
+                            bool ok = true;
+                            if (P.check_finite) {
+#pragma unroll
+                                for (int k = 0; k < N; ++k) ok = ok && isfinite(xs[k]);
+                            }
+                            const float nx = xs[0], ny = xs[1], nz = TWO_D ? 0.0f : xs[2];
+                            const bool inb = within_bounds<MODEL>(P, xs);
+                            const bool hit = in_obstacle(P, E, nx, ny, nz, c[4], c[5]);
+                            ok = ok && inb && !hit;
+                            const float dx = nx - px, dy = ny - py, dz = nz - pz;
+                            float d2 = dx * dx;
+                            d2 = fmaf(dy, dy, d2);
+                            if (!TWO_D) d2 = fmaf(dz, dz, d2);
+                            const float d = sqrtf(d2);
+                            if (ok && d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, c[3], c[4], c[5]))
+                                ok = false;
+                            if (!ok) bad[pi] = 1u;
+                            run += len_fixed(d);
+                            ppx = nx; ppy = ny; ppz = nz;
+                            prev_s = s;
+                        }
+                    }
+                    flush(pi);
+            }
             }
             __syncthreads();
             // (4) owner thread: path length in sample order, region, admission
@@ -605,7 +668,8 @@ __global__ void __launch_bounds__(PropCfg<MODEL>::T, PropCfg<MODEL>::MIN_BLOCKS)
         // small launches are latency-bound: flatten them into samples; large
         // ones are issue-bound, where the step-sorted path runs fewer instructions
         if (P.flat_on && B.ctl->n_items <= P.flat_max) {
-            flat_phase<MODEL>(P, B, E, dyn);
+            if (P.flat_il) flat_phase<MODEL, true>(P, B, E, dyn);
+            else flat_phase<MODEL, false>(P, B, E, dyn);
             return;
         }
     }
@@ -1363,7 +1427,9 @@ void plan_propagate_smem(KpProblem& P) {
         const uint32_t rw = static_cast<uint32_t>((P.n + P.m + 2 + 3) / 4);
         const size_t rec = pad16(static_cast<size_t>(nb) * rw * 16);
         const size_t offs = pad16((T + 1) * 4ull), badb = pad16(T * 4ull), lenb = pad16(2 * T * 4ull);
-        const size_t flat = rec + offs + badb + lenb;
+        const uint32_t smax = static_cast<uint32_t>(std::ceil(static_cast<double>(P.t_prop) / P.h)) + 1u;
+        const size_t idxb = pad16((static_cast<size_t>(nb) * smax / 32 + 2) * 2);
+        const size_t flat = rec + offs + badb + lenb + idxb;
         if (base + flat <= 96 * 1024) {
             P.flat_on = 1;
             P.flat_nb = nb;
@@ -1371,6 +1437,14 @@ void plan_propagate_smem(KpProblem& P) {
             P.flat_offs = static_cast<uint32_t>(base + rec);
             P.flat_bad = static_cast<uint32_t>(base + rec + offs);
             P.flat_len = static_cast<uint32_t>(base + rec + offs + badb);
+            P.flat_idx = static_cast<uint32_t>(base + rec + offs + badb + lenb);
+            // sample-to-thread mapping: interleaved (a warp's lanes on consecutive
+            // samples of a few items: coherent obstacle lookups) for rollouts of
+            // up to 32 samples; contiguous runs per thread (previous sample
+            // carried, one record load and one length update per run) for longer
+            // ones, where they measured faster (profiles/README.md)
+            const char* il = std::getenv("KP_FLAT_IL");
+            P.flat_il = il ? (il[0] != '0') : (smax <= 32 ? 1 : 0);
             area = std::max(area, flat);
         }
     }

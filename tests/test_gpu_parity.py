@@ -220,21 +220,23 @@ def test_whole_run_bit_identical_steady_state(scene, iters):
         _compare_runs(g, o, rg, ro)
 
 
-@pytest.mark.parametrize("mode", ["sample_parallel", "step_sorted"])
+@pytest.mark.parametrize("mode", ["interleaved", "runs", "step_sorted"])
 @pytest.mark.parametrize("scene,iters", [("forest_di6", 24), ("zigzag2d", 40)])
 def test_whole_run_bit_identical_propagate_paths(scene, iters, mode, monkeypatch):
-    """The double integrator's two propagate paths (kp_kernels.cu flat_phase for
-    small launches, the step-sorted path for large ones) each reproduce the
-    restatement on their own: forced for every launch size here."""
-    if mode == "sample_parallel":
-        monkeypatch.setenv("KP_FLAT_MAX", str(1 << 30))
-    else:
+    """The double integrator's propagate paths (kp_kernels.cu flat_phase with
+    interleaved samples or contiguous runs per thread for one-wave launches,
+    the step-sorted path for larger ones) each reproduce the restatement on
+    their own: forced for every launch size here."""
+    if mode == "step_sorted":
         monkeypatch.setenv("KP_FLAT", "0")
+    else:
+        monkeypatch.setenv("KP_FLAT_MAX", str(1 << 30))
+        monkeypatch.setenv("KP_FLAT_IL", "1" if mode == "interleaved" else "0")
     s = scenarios.load(scene)
     with Planner(s, seed=21) as g:
         rg = g.solve(budget_s=0.0, max_iterations=iters)
-    monkeypatch.delenv("KP_FLAT_MAX", raising=False)
-    monkeypatch.delenv("KP_FLAT", raising=False)
+    for k in ("KP_FLAT_MAX", "KP_FLAT", "KP_FLAT_IL"):
+        monkeypatch.delenv(k, raising=False)
     o = kpo.Oracle(s, kpo.MIRROR32, seed=21, workers=8)
     ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
     for k in ("best_cost", "node_count", "propagations_valid", "nodes_committed", "timeline_len"):
