@@ -354,17 +354,20 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
 }
 
 // Sample-parallel propagate for the double integrator (closed form, §4 of
-// DESIGN.md).  Its samples do not depend on one another, so a batch of up to
-// flat_nb work items is flattened into its samples and every thread of the
-// block checks a contiguous run of them: the batch takes about
+// DESIGN.md), used for one-wave launches (at most flat_nb items per block).
+// Its samples do not depend on one another, so a batch of items is flattened
+// into its samples and the whole block checks them: the batch takes about
 // (sum of step counts) / threads rounds instead of the longest item's step
 // count, which bounds a one-wave launch in the step-sorted path.  Per batch:
 // (1) one item per thread draws (u, dt), stages the parent state and counts
 // its samples; (2) block scan of the counts; (3) sample checks (bounds,
-// obstacles, interpolated points, segment length into dd[]); an item with a
-// failed sample is flagged and its remaining samples skipped; (4) the owner
-// thread sums its segment lengths in sample order (the sequential recipe's
-// order, so the cost is bit-identical) and admits the candidate.
+// obstacles, interpolated points) and segment lengths, IL: interleaved over
+// the block (a warp's lanes on consecutive samples of a few items: coherent
+// obstacle lookups), else a contiguous run per thread (long rollouts); an
+// item with a failed sample is flagged and its remaining samples skipped;
+// segment lengths go into the item's fixed-point path length (order-
+// independent, §4); (4) the owner thread converts the length, computes region
+// and goal, and admits the candidate.
 template <int MODEL, bool IL>
 KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, unsigned char* dyn) {
     constexpr int N = Model<MODEL>::N;
@@ -389,7 +392,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
     if (done) return;
     if (threadIdx.x < 6) fcnt[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
-    const uint32_t FB = P.flat_nb;  // items per batch (T, or T / 2 for long rollouts)
+    const uint32_t FB = P.flat_nb;  // items per batch
     const uint32_t CH = min(T * PropCfg<MODEL>::MAXG, ((n_items + gridDim.x - 1) / gridDim.x + 31u) & ~31u);
     const uint32_t n_chunks = (n_items + CH - 1) / CH;
     if (blockIdx.x >= n_chunks) return;
