@@ -353,6 +353,10 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     count_flush(ctl, c, sh.cnt, lane);
 }
 
+#ifndef KP_FLAT_ITEMS
+#define KP_FLAT_ITEMS 512u  // items per sample-parallel batch (a multiple of the block size)
+#endif
+
 // Sample-parallel propagate for the double integrator (closed form, §4 of
 // DESIGN.md), used for one-wave launches (at most flat_nb items per block).
 // Its samples do not depend on one another, so a batch of items is flattened
@@ -374,25 +378,26 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
     constexpr int M = Model<MODEL>::M;
     constexpr uint32_t T = PropCfg<MODEL>::T;
     constexpr uint32_t NWARP = T / 32;
+    constexpr uint32_t IPT = (KP_FLAT_ITEMS + T - 1) / T;  // items per thread in a batch
+    constexpr uint32_t FB = IPT * T;                        // items per batch (== P.flat_nb)
     constexpr int RW = (N + M + 2 + 3) / 4;  // float4 words per item record: x0, u, dt, S
     constexpr bool TWO_D = (MODEL == 0);
     __shared__ unsigned long long fcnt[6];
     __shared__ uint32_t wsum[NWARP];
     __shared__ uint32_t fchunk;
     float4* const rec = reinterpret_cast<float4*>(dyn + P.flat_rec);
-    uint32_t* const off = reinterpret_cast<uint32_t*>(dyn + P.flat_offs);           // [T + 1]
-    volatile uint32_t* const bad = reinterpret_cast<uint32_t*>(dyn + P.flat_bad);   // [T]
+    uint32_t* const off = reinterpret_cast<uint32_t*>(dyn + P.flat_offs);           // [FB + 1]
+    volatile uint32_t* const bad = reinterpret_cast<uint32_t*>(dyn + P.flat_bad);   // [FB]
     // fixed-point path lengths as two 32-bit limbs (native shared atomics):
     // len = hi << 24 + lo, every run adding its low 24 bits to lo and the rest to hi
-    uint32_t* const len_lo = reinterpret_cast<uint32_t*>(dyn + P.flat_len);  // [T]
-    uint32_t* const len_hi = len_lo + T;                                    // [T]
+    uint32_t* const len_lo = reinterpret_cast<uint32_t*>(dyn + P.flat_len);  // [FB]
+    uint32_t* const len_hi = len_lo + FB;                                   // [FB]
     KpCtl* ctl = B.ctl;
     const uint32_t done = ctl->done, n_items = ctl->n_items, it = ctl->iter;
     const unsigned long long seed = ctl->seed;
     if (done) return;
     if (threadIdx.x < 6) fcnt[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
-    const uint32_t FB = P.flat_nb;  // items per batch
     const uint32_t CH = min(T * PropCfg<MODEL>::MAXG, ((n_items + gridDim.x - 1) / gridDim.x + 31u) & ~31u);
     const uint32_t n_chunks = (n_items + CH - 1) / CH;
     if (blockIdx.x >= n_chunks) return;
@@ -408,40 +413,48 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
         if (chunk >= n_chunks) break;
         const uint32_t cend = min(chunk * CH + CH, n_items);
         for (uint32_t b0 = chunk * CH; b0 < cend; b0 += FB) {
-            // (1) one item per thread: draw (u, dt), stage the parent state
-            const uint32_t i = b0 + threadIdx.x;
-            const bool have = threadIdx.x < FB && i < cend;
-            uint32_t node = 0, seff = 0;
-            float acc_p = 0.0f;
-            if (have) {
-                const uint32_t f = i / lam;
-                const uint32_t br = i - f * lam;
-                KP_ASSERT(f < ctl->n_va, 10);
-                node = va[f];
-                KP_ASSERT(node < ctl->n_nodes, 11);
-                float r[RW * 4];
+            // (1) IPT consecutive items per thread: draw (u, dt), stage the parent state
+            uint32_t node[IPT], seffk[IPT];
+            float acc_p[IPT];
+            uint32_t seff = 0;  // this thread's samples
 #pragma unroll
-                for (int w = 0; w < RW * 4; ++w) r[w] = 0.0f;
+            for (uint32_t k = 0; k < IPT; ++k) {
+                const uint32_t p = threadIdx.x * IPT + k;
+                const uint32_t i = b0 + p;
+                node[k] = 0;
+                seffk[k] = 0;
+                acc_p[k] = 0.0f;
+                if (i < cend) {
+                    const uint32_t f = i / lam;
+                    const uint32_t br = i - f * lam;
+                    KP_ASSERT(f < ctl->n_va, 10);
+                    node[k] = va[f];
+                    KP_ASSERT(node[k] < ctl->n_nodes, 11);
+                    float r[RW * 4];
 #pragma unroll
-                for (int d = 0; d < N; ++d) r[d] = B.state[static_cast<size_t>(d) * cap + node];
-                acc_p = __uint_as_float(B.acc[node]);
-                float u[M], dt;
-                sample_item<M>(P, seed, it, node, br, u, dt);
-                const int S = step_count(P, dt);
-                // the shortened last step may be empty (dt - (S-1) h <= 0): then
-                // the rollout ends at sample S - 1 (as integrate_steps)
-                seff = static_cast<uint32_t>((S > 1 && !(dt - static_cast<float>(S - 1) * P.h > 0.0f)) ? S - 1 : S);
+                    for (int w = 0; w < RW * 4; ++w) r[w] = 0.0f;
 #pragma unroll
-                for (int d = 0; d < M; ++d) r[N + d] = u[d];
-                r[N + M] = dt;
-                r[N + M + 1] = __int_as_float(S);
+                    for (int d = 0; d < N; ++d) r[d] = B.state[static_cast<size_t>(d) * cap + node[k]];
+                    acc_p[k] = __uint_as_float(B.acc[node[k]]);
+                    float u[M], dt;
+                    sample_item<M>(P, seed, it, node[k], br, u, dt);
+                    const int S = step_count(P, dt);
+                    // the shortened last step may be empty (dt - (S-1) h <= 0): then
+                    // the rollout ends at sample S - 1 (as integrate_steps)
+                    seffk[k] = static_cast<uint32_t>((S > 1 && !(dt - static_cast<float>(S - 1) * P.h > 0.0f)) ? S - 1 : S);
 #pragma unroll
-                for (int w = 0; w < RW; ++w)
-                    rec[threadIdx.x * RW + w] = make_float4(r[4 * w], r[4 * w + 1], r[4 * w + 2], r[4 * w + 3]);
+                    for (int d = 0; d < M; ++d) r[N + d] = u[d];
+                    r[N + M] = dt;
+                    r[N + M + 1] = __int_as_float(S);
+#pragma unroll
+                    for (int w = 0; w < RW; ++w)
+                        rec[p * RW + w] = make_float4(r[4 * w], r[4 * w + 1], r[4 * w + 2], r[4 * w + 3]);
+                }
+                seff += seffk[k];
+                bad[p] = 0u;
+                len_lo[p] = 0u;
+                len_hi[p] = 0u;
             }
-            bad[threadIdx.x] = 0u;
-            len_lo[threadIdx.x] = 0u;
-            len_hi[threadIdx.x] = 0u;
             // (2) exclusive scan of the sample counts over the block
             uint32_t x = seff;
 #pragma unroll
@@ -462,17 +475,30 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
             }
             __syncthreads();
             const uint32_t excl = x - seff + (warp ? wsum[warp - 1] : 0u);
-            off[threadIdx.x] = excl;
-            if (threadIdx.x == T - 1) off[T] = excl + seff;
+            {
+                uint32_t o = excl;
+#pragma unroll
+                for (uint32_t k = 0; k < IPT; ++k) {
+                    off[threadIdx.x * IPT + k] = o;
+                    o += seffk[k];
+                }
+                if (threadIdx.x == T - 1) off[FB] = o;
+            }
             __syncthreads();
             if constexpr (IL) {
                 // (3) samples interleaved over the block: round r, thread t checks
                 // sample r*T + t, so a warp's lanes hold consecutive samples of a
                 // few items (nearby points: coherent broad / narrow phases)
-                const uint32_t U = off[T];
+                const uint32_t U = off[FB];
                 uint16_t* const idx = reinterpret_cast<uint16_t*>(dyn + P.flat_idx);  // item of sample 32k
-                if (seff) {
-                    for (uint32_t m = (excl + 31) >> 5; (m << 5) < excl + seff; ++m) idx[m] = static_cast<uint16_t>(threadIdx.x);
+                {
+                    uint32_t o = excl;
+#pragma unroll
+                    for (uint32_t k = 0; k < IPT; ++k) {
+                        for (uint32_t m = (o + 31) >> 5; (m << 5) < o + seffk[k]; ++m)
+                            idx[m] = static_cast<uint16_t>(threadIdx.x * IPT + k);
+                        o += seffk[k];
+                    }
                 }
                 __syncthreads();
                 for (uint32_t q0 = 0; q0 < U; q0 += T) {
@@ -528,11 +554,11 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 }
             } else {
                 // (3) a contiguous run of samples per thread
-                const uint32_t U = off[T];
+                const uint32_t U = off[FB];
                 const uint32_t qa = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x) * U) / T);
                 const uint32_t qb = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x + 1) * U) / T);
                 if (qa < qb) {
-                    uint32_t lo = 0, hi = T;  // off[lo] <= qa < off[hi]
+                    uint32_t lo = 0, hi = FB;  // off[lo] <= qa < off[hi]
                     while (hi - lo > 1) {
                         const uint32_t mid = (lo + hi) >> 1;
                         if (off[mid] <= qa) lo = mid;
@@ -615,12 +641,16 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
             }
             }
             __syncthreads();
-            // (4) owner thread: path length in sample order, region, admission
-            if (have && !bad[threadIdx.x]) {
+            // (4) owner thread: path length, region, admission
+#pragma unroll
+            for (uint32_t k = 0; k < IPT; ++k) {
+                const uint32_t p = threadIdx.x * IPT + k;
+                const uint32_t i = b0 + p;
+                if (!(i < cend) || bad[p]) continue;
                 float r[RW * 4];
 #pragma unroll
                 for (int w = 0; w < RW; ++w) {
-                    const float4 v = rec[threadIdx.x * RW + w];
+                    const float4 v = rec[p * RW + w];
                     r[4 * w] = v.x; r[4 * w + 1] = v.y; r[4 * w + 2] = v.z; r[4 * w + 3] = v.w;
                 }
                 float x0[N], u[M], xs[N];
@@ -630,10 +660,10 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 for (int d = 0; d < M; ++d) u[d] = r[N + d];
                 const float dt = r[N + M];
                 const int S = __float_as_int(r[N + M + 1]);
-                di_sample<MODEL>(x0, u, (static_cast<int>(seff) == S) ? dt : static_cast<float>(seff) * P.h, xs);
+                di_sample<MODEL>(x0, u, (static_cast<int>(seffk[k]) == S) ? dt : static_cast<float>(seffk[k]) * P.h, xs);
                 ItemOut o;
-                const long long fx = (static_cast<long long>(len_hi[threadIdx.x]) << 24) + len_lo[threadIdx.x];
-                finish_item<MODEL>(P, xs, dt, fixed_len(fx), acc_p, o);
+                const long long fx = (static_cast<long long>(len_hi[p]) << 24) + len_lo[p];
+                finish_item<MODEL>(P, xs, dt, fixed_len(fx), acc_p[k], o);
                 ++c[0];
                 const uint32_t bits = __float_as_uint(o.acc);
                 KP_ASSERT(o.region < P.n_regions, 12);
@@ -1406,9 +1436,6 @@ size_t propagate_smem(const KpProblem& P) { return P.prop_smem; }
 // under PDL).  A sample-parallel batch holds KP_FLAT_ITEMS item records,
 // sample offsets, invalid flags and fixed-point path lengths.  KP_FLAT=0
 // turns the sample-parallel path off.
-#ifndef KP_FLAT_ITEMS
-#define KP_FLAT_ITEMS 512u
-#endif
 void plan_propagate_smem(KpProblem& P) {
     auto pad16 = [](size_t b) { return (b + 15) & ~static_cast<size_t>(15); };
     size_t seq = 0;
@@ -1426,10 +1453,10 @@ void plan_propagate_smem(KpProblem& P) {
     P.flat_max = 0;
     const char* env = std::getenv("KP_FLAT");
     if ((P.model == 0 || P.model == 1) && !(env && env[0] == '0')) {
-        const uint32_t nb = std::min<uint32_t>(KP_FLAT_ITEMS, T);
+        const uint32_t nb = (KP_FLAT_ITEMS + T - 1) / T * T;
         const uint32_t rw = static_cast<uint32_t>((P.n + P.m + 2 + 3) / 4);
         const size_t rec = pad16(static_cast<size_t>(nb) * rw * 16);
-        const size_t offs = pad16((T + 1) * 4ull), badb = pad16(T * 4ull), lenb = pad16(2 * T * 4ull);
+        const size_t offs = pad16((nb + 1) * 4ull), badb = pad16(nb * 4ull), lenb = pad16(2 * nb * 4ull);
         const uint32_t smax = static_cast<uint32_t>(std::ceil(static_cast<double>(P.t_prop) / P.h)) + 1u;
         const size_t idxb = pad16((static_cast<size_t>(nb) * smax / 32 + 2) * 2);
         const size_t flat = rec + offs + badb + lenb + idxb;
