@@ -887,7 +887,18 @@ KP_DEV SelLayout sel_layout(uint32_t n_live, uint32_t n_items, uint32_t n_adm) {
 
 KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
     KpCtl* ctl = B.ctl;
-    // every control-block read up front: one round trip
+    // every control-block read up front: one round trip; beside it, the first
+    // tile's live entries of both list parities (the parity comes with the
+    // control block), so the region-cost gather follows the first round trip
+    const uint32_t e0 = blockIdx.x * KP_SELECT_THREADS + threadIdx.x;
+    uint4 rec_a = make_uint4(0u, 0u, 0u, 0u), rec_b = rec_a;
+    uint32_t si_a = 0u, si_b = 0u;
+    if (e0 < P.capacity) {
+        rec_a = B.live[0][e0];
+        rec_b = B.live[1][e0];
+        si_a = B.live_si[0][e0];
+        si_b = B.live_si[1][e0];
+    }
     const uint32_t done = ctl->done, it = ctl->iter, n_live = ctl->n_live, n_items = ctl->n_items;
     const uint32_t n_adm = ctl->n_adm_iter;
     if (done) return;
@@ -909,7 +920,10 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
         Cnt3 x{0, 0, 0};
         if (e < n_live) {
             ++nlive;
-            const uint32_t si = prune_node(P, B, live[e], live_si[e], &term, &deact, &react, &hops);
+            const bool first = tile == blockIdx.x;
+            const bool odd = (it & 1u) != 0u;
+            const uint32_t si = prune_node(P, B, first ? (odd ? rec_b : rec_a) : live[e],
+                                           first ? (odd ? si_b : si_a) : live_si[e], &term, &deact, &react, &hops);
             B.live_st[e] = si;  // scatter reads it by position, in parallel with live[e]
             const uint32_t st = si & 0xFFu;
             x.k = st != KP_ST_TERMINAL;
