@@ -643,6 +643,7 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         void* hc = nullptr;
         cuda_check(cudaHostAlloc(&hc, sizeof(KpCtl), cudaHostAllocDefault), "cudaHostAlloc ctl");
         pl->h_ctl = static_cast<KpCtl*>(hc);
+        pl->P.sel_spec = 1;
         kp::plan_propagate_smem(pl->P);
         cuda_check(kp::set_propagate_smem(P), "smem attribute");
         const int occ = std::max(1, kp::propagate_occupancy(P));
@@ -953,6 +954,7 @@ int kp_batch_create(const kp_problem_desc* problem, const kp_config_desc* config
                 pl->grid_prop = std::max(std::max(1, pl->sms / 2), pl->grid_prop * 4 / lanes);
                 pl->grid_sel = std::max(std::max(1, pl->sms / 2), pl->grid_sel * 4 / lanes);
                 kp::set_flat_limit(pl->P, pl->grid_prop);
+                pl->P.sel_spec = 0;  // throughput-bound: the speculative loads cost more than they hide
                 if (pl->graph) cudaGraphExecDestroy(pl->graph);
                 pl->graph = nullptr;
                 capture_graph(pl);

@@ -885,6 +885,7 @@ KP_DEV SelLayout sel_layout(uint32_t n_live, uint32_t n_items, uint32_t n_adm) {
     return l;
 }
 
+template <bool SPEC>
 KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
     KpCtl* ctl = B.ctl;
     // every control-block read up front: one round trip; beside it, the first
@@ -893,7 +894,7 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
     const uint32_t e0 = blockIdx.x * KP_SELECT_THREADS + threadIdx.x;
     uint4 rec_a = make_uint4(0u, 0u, 0u, 0u), rec_b = rec_a;
     uint32_t si_a = 0u, si_b = 0u;
-    if (e0 < P.capacity) {
+    if (SPEC && e0 < P.capacity) {
         rec_a = B.live[0][e0];
         rec_b = B.live[1][e0];
         si_a = B.live_si[0][e0];
@@ -920,7 +921,7 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
         Cnt3 x{0, 0, 0};
         if (e < n_live) {
             ++nlive;
-            const bool first = tile == blockIdx.x;
+            const bool first = SPEC && tile == blockIdx.x;
             const bool odd = (it & 1u) != 0u;
             const uint32_t si = prune_node(P, B, first ? (odd ? rec_b : rec_a) : live[e],
                                            first ? (odd ? si_b : si_a) : live_si[e], &term, &deact, &react, &hops);
@@ -1007,10 +1008,14 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
     }
 }
 
-__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_reduce(KpProblem P, KpBuffers B) {
+// SPEC: the first tile's live entries are loaded beside the control block
+// (a lone query's latency win; the batch engine's concurrent lanes use the
+// plain variant, which also needs fewer registers)
+template <bool SPEC>
+__global__ void __launch_bounds__(KP_SELECT_THREADS, SPEC ? 5 : 8) k_select_reduce(KpProblem P, KpBuffers B) {
     pdl_wait();
     pdl_trigger();
-    select_reduce_phase(P, B);
+    select_reduce_phase<SPEC>(P, B);
 }
 
 // Close an iteration: counts, stats, best / timeline / TTFS
@@ -1543,7 +1548,8 @@ cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_pr
         if (e != cudaSuccess) return e;
     }
     if (which & 2) {
-        e = launch_k(k_select_reduce, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
+        e = P.sel_spec ? launch_k(k_select_reduce<true>, grid_sel, KP_SELECT_THREADS, 0, st, P, B)
+                       : launch_k(k_select_reduce<false>, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
         if (e != cudaSuccess) return e;
     }
     if (which & 4) e = launch_k(k_select_scatter, grid_sel, KP_SELECT_THREADS, 0, st, P, B);

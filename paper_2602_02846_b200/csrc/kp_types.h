@@ -85,6 +85,8 @@ struct KpProblem {
     uint32_t seq_base;         // step-sorted path: PropSmem<MODEL>
     // sample-parallel path (double integrator, kp_kernels.cu flat_phase): item
     // records, sample offsets, invalid flags, fixed-point path lengths
+    int32_t sel_spec;          // select_reduce loads its first tile's live entries before the control block
+                               // (latency win for a lone query; off for concurrent batch lanes)
     int32_t flat_on;
     uint32_t flat_max;         // launches of at most this many items take the sample-parallel path
     uint32_t flat_nb;          // items per batch
