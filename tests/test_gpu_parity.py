@@ -221,7 +221,7 @@ def test_whole_run_bit_identical_steady_state(scene, iters):
 
 
 @pytest.mark.parametrize("mode", ["interleaved", "runs", "step_sorted"])
-@pytest.mark.parametrize("scene,iters", [("forest_di6", 24), ("zigzag2d", 40)])
+@pytest.mark.parametrize("scene,iters", [("forest_di6", 24), ("zigzag2d", 40), ("building6d", 20)])
 def test_whole_run_bit_identical_propagate_paths(scene, iters, mode, monkeypatch):
     """The double integrator's propagate paths (kp_kernels.cu flat_phase with
     interleaved samples or contiguous runs per thread for one-wave launches,
