@@ -153,6 +153,17 @@ def _init_ranks(ws: int, local: int):
     return dev_idx, torch.device("cuda", dev_idx)
 
 
+def _cpu_model():
+    """Host CPU model (the CPU baseline states its cores and model)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def _median(xs):
     xs = [x for x in xs if x == x]
     return statistics.median(xs) if xs else None
@@ -198,6 +209,7 @@ def run_reference(args, scenario):
         "metrics": {"ms_to_first_solution_median": _median(ttfs), "solution_cost_at_budget_median": _median(costs),
                     "success_rate": found / args.steps, "node_propagations_per_sec": value},
         "cpu_baseline": {"value": value, "unit": "propagations/s", "cores": cores, "kind": "port",
+                         "cpu_model": _cpu_model(),
                          "sample": f"{args.steps} queries x {args.budget_ms} ms budget, fp64 restatement "
                                    f"(oracle/kpo.hpp Faithful64, SplitMix64), {cores} worker threads"},
         "e2e": {"value": value, "unit": "propagations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -318,6 +330,7 @@ def run_b200(args, scenario):
             p1 += r["propagations_attempted"]
             w1 += r["wall_s"]
         cpu = {"value": props / wall, "unit": "propagations/s", "cores": cores, "kind": "port",
+               "cpu_model": _cpu_model(),
                "sample": f"{args.config}, {n_q} queries (seeds {qs[0]}..{qs[-1]}) "
                          f"x {args.cpu_query_s:g} s budget each on {cores} threads, fp64 restatement "
                          "(oracle Faithful64, SplitMix64)",
