@@ -356,6 +356,9 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
 #ifndef KP_FLAT_ITEMS
 #define KP_FLAT_ITEMS 512u  // items per sample-parallel batch (a multiple of the block size)
 #endif
+#ifndef KP_IDX_STEP
+#define KP_IDX_STEP 8u      // samples per entry of the interleaved path's sample -> item index
+#endif
 
 // Sample-parallel propagate for the double integrator (closed form, §4 of
 // DESIGN.md), used for one-wave launches (at most flat_nb items per block).
@@ -490,12 +493,12 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 // sample r*T + t, so a warp's lanes hold consecutive samples of a
                 // few items (nearby points: coherent broad / narrow phases)
                 const uint32_t U = off[FB];
-                uint16_t* const idx = reinterpret_cast<uint16_t*>(dyn + P.flat_idx);  // item of sample 32k
+                uint16_t* const idx = reinterpret_cast<uint16_t*>(dyn + P.flat_idx);  // item of sample KP_IDX_STEP * k
                 {
                     uint32_t o = excl;
 #pragma unroll
                     for (uint32_t k = 0; k < IPT; ++k) {
-                        for (uint32_t m = (o + 31) >> 5; (m << 5) < o + seffk[k]; ++m)
+                        for (uint32_t m = (o + KP_IDX_STEP - 1) / KP_IDX_STEP; m * KP_IDX_STEP < o + seffk[k]; ++m)
                             idx[m] = static_cast<uint16_t>(threadIdx.x * IPT + k);
                         o += seffk[k];
                     }
@@ -504,7 +507,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 for (uint32_t q0 = 0; q0 < U; q0 += T) {
                     const uint32_t q = q0 + threadIdx.x;
                     if (q >= U) break;
-                    uint32_t pi = idx[q >> 5];
+                    uint32_t pi = idx[q / KP_IDX_STEP];
                     while (off[pi + 1] <= q) ++pi;
                     if (bad[pi]) continue;
                     float x0[N], u[M];
@@ -1477,7 +1480,7 @@ void plan_propagate_smem(KpProblem& P) {
         const size_t rec = pad16(static_cast<size_t>(nb) * rw * 16);
         const size_t offs = pad16((nb + 1) * 4ull), badb = pad16(nb * 4ull), lenb = pad16(2 * nb * 4ull);
         const uint32_t smax = static_cast<uint32_t>(std::ceil(static_cast<double>(P.t_prop) / P.h)) + 1u;
-        const size_t idxb = pad16((static_cast<size_t>(nb) * smax / 32 + 2) * 2);
+        const size_t idxb = pad16((static_cast<size_t>(nb) * smax / KP_IDX_STEP + 2) * 2);
         const size_t flat = rec + offs + badb + lenb + idxb;
         if (base + flat <= 96 * 1024) {
             P.flat_on = 1;
