@@ -241,3 +241,26 @@ def test_whole_run_bit_identical_propagate_paths(scene, iters, mode, monkeypatch
     ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
     for k in ("best_cost", "node_count", "propagations_valid", "nodes_committed", "timeline_len"):
         assert rg[k] == ro[k], (k, rg[k], ro[k])
+
+
+@pytest.mark.parametrize("t_prop,h,lam", [(0.02, 0.02, 32), (2.0, 0.02, 4), (0.5, 0.02, 1)])
+@pytest.mark.parametrize("mode", ["interleaved", "runs", "step_sorted"])
+def test_whole_run_bit_identical_rollout_lengths(t_prop, h, lam, mode, monkeypatch):
+    """Rollout-length extremes on the double integrator's propagate paths: one
+    sample per rollout (t_prop = h), up to 101 samples (past the interleaved
+    path's 32-sample default and the step-count sort's 64 buckets), lambda = 1."""
+    if mode == "step_sorted":
+        monkeypatch.setenv("KP_FLAT", "0")
+    else:
+        monkeypatch.setenv("KP_FLAT_MAX", str(1 << 30))
+        monkeypatch.setenv("KP_FLAT_IL", "1" if mode == "interleaved" else "0")
+    s = scenarios.load("forest_di6", t_prop=t_prop, ode_step=h, collision_step=0.05, **{"lambda": lam})
+    iters = 12
+    with Planner(s, seed=3) as g:
+        rg = g.solve(budget_s=0.0, max_iterations=iters)
+    for k in ("KP_FLAT_MAX", "KP_FLAT", "KP_FLAT_IL"):
+        monkeypatch.delenv(k, raising=False)
+    o = kpo.Oracle(s, kpo.MIRROR32, seed=3, workers=8)
+    ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
+    for k in ("best_cost", "node_count", "propagations_valid", "nodes_committed", "timeline_len"):
+        assert rg[k] == ro[k], (k, rg[k], ro[k])
