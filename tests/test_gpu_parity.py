@@ -264,3 +264,18 @@ def test_whole_run_bit_identical_rollout_lengths(t_prop, h, lam, mode, monkeypat
     ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
     for k in ("best_cost", "node_count", "propagations_valid", "nodes_committed", "timeline_len"):
         assert rg[k] == ro[k], (k, rg[k], ro[k])
+
+
+def test_quadcopter_split_long_rollouts(monkeypatch):
+    """Quadcopter split rollouts (first pass of 8 steps, parked survivors) with
+    rollouts of up to 51 steps and several groups per warp (small grid)."""
+    monkeypatch.setenv("KP_PROP_GRID", "12")
+    s = scenarios.load("building_quad12", t_prop=1.0, **{"lambda": 8})
+    iters = 10
+    with Planner(s, seed=4) as g:
+        rg = g.solve(budget_s=0.0, max_iterations=iters)
+    monkeypatch.delenv("KP_PROP_GRID")
+    o = kpo.Oracle(s, kpo.MIRROR32, seed=4, workers=16)
+    ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
+    for k in ("best_cost", "node_count", "propagations_valid", "nodes_committed", "timeline_len"):
+        assert rg[k] == ro[k], (k, rg[k], ro[k])
