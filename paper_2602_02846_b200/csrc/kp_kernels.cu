@@ -353,6 +353,35 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
     count_flush(ctl, c, sh.cnt, lane);
 }
 
+// One sample of a closed-form rollout (the sequential loop's per-step checks,
+// integrate_steps): finite state (when a bound is infinite), state bounds,
+// obstacles, and the interpolated points of the segment from the previous
+// sample position (px, py, pz); d = the segment length.  c: the work
+// counters (samples, interpolated points, box / sphere tests at 2..5).
+template <int MODEL>
+KP_DEV bool check_sample(const KpProblem& P, const Env& E, const float* xs, float px, float py, float pz, float& d,
+                         uint32_t* c) {
+    constexpr int N = Model<MODEL>::N;
+    constexpr bool TWO_D = (MODEL == 0);
+    ++c[2];
+    bool ok = true;
+    if (P.check_finite) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) ok = ok && isfinite(xs[k]);
+    }
+    const float nx = xs[0], ny = xs[1], nz = TWO_D ? 0.0f : xs[2];
+    const bool inb = within_bounds<MODEL>(P, xs);
+    const bool hit = in_obstacle(P, E, nx, ny, nz, c[4], c[5]);
+    ok = ok && inb && !hit;
+    const float dx = nx - px, dy = ny - py, dz = nz - pz;
+    float d2 = dx * dx;
+    d2 = fmaf(dy, dy, d2);
+    if (!TWO_D) d2 = fmaf(dz, dz, d2);
+    d = sqrtf(d2);
+    if (ok && d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, c[3], c[4], c[5])) ok = false;
+    return ok;
+}
+
 #ifndef KP_FLAT_ITEMS
 #define KP_FLAT_ITEMS 512u  // items per sample-parallel batch (a multiple of the block size)
 #endif
@@ -533,24 +562,8 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                         di_sample<MODEL>(x0, u, static_cast<float>(s - 1) * P.h, xp);
                     }
                     const float px = xp[0], py = xp[1], pz = TWO_D ? 0.0f : xp[2];
-                    ++c[2];
-                    bool ok = true;
-                    if (P.check_finite) {
-#pragma unroll
-                        for (int k = 0; k < N; ++k) ok = ok && isfinite(xs[k]);
-                    }
-                    const float nx = xs[0], ny = xs[1], nz = TWO_D ? 0.0f : xs[2];
-                    const bool inb = within_bounds<MODEL>(P, xs);
-                    const bool hit = in_obstacle(P, E, nx, ny, nz, c[4], c[5]);
-                    ok = ok && inb && !hit;
-                    const float dx = nx - px, dy = ny - py, dz = nz - pz;
-                    float d2 = dx * dx;
-                    d2 = fmaf(dy, dy, d2);
-                    if (!TWO_D) d2 = fmaf(dz, dz, d2);
-                    const float d = sqrtf(d2);
-                    if (ok && d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, c[3], c[4], c[5]))
-                        ok = false;
-                    if (!ok) bad[pi] = 1u;
+                    float d;
+                    if (!check_sample<MODEL>(P, E, xs, px, py, pz, d, c)) bad[pi] = 1u;
                     const long long fx = len_fixed(d);
                     atomicAdd(len_lo + pi, static_cast<uint32_t>(fx & 0xFFFFFF));
                     atomicAdd(len_hi + pi, static_cast<uint32_t>(fx >> 24));
@@ -617,26 +630,10 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                                 di_sample<MODEL>(x0, u, static_cast<float>(s - 1) * P.h, xp);
                                 px = xp[0]; py = xp[1]; pz = TWO_D ? 0.0f : xp[2];
                             }
-                            ++c[2];
-                            bool ok = true;
-                            if (P.check_finite) {
-#pragma unroll
-                                for (int k = 0; k < N; ++k) ok = ok && isfinite(xs[k]);
-                            }
-                            const float nx = xs[0], ny = xs[1], nz = TWO_D ? 0.0f : xs[2];
-                            const bool inb = within_bounds<MODEL>(P, xs);
-                            const bool hit = in_obstacle(P, E, nx, ny, nz, c[4], c[5]);
-                            ok = ok && inb && !hit;
-                            const float dx = nx - px, dy = ny - py, dz = nz - pz;
-                            float d2 = dx * dx;
-                            d2 = fmaf(dy, dy, d2);
-                            if (!TWO_D) d2 = fmaf(dz, dz, d2);
-                            const float d = sqrtf(d2);
-                            if (ok && d2 > P.coll_d2 && segment_hit<TWO_D>(P, E, px, py, pz, dx, dy, dz, d, c[3], c[4], c[5]))
-                                ok = false;
-                            if (!ok) bad[pi] = 1u;
+                            float d;
+                            if (!check_sample<MODEL>(P, E, xs, px, py, pz, d, c)) bad[pi] = 1u;
                             run += len_fixed(d);
-                            ppx = nx; ppy = ny; ppz = nz;
+                            ppx = xs[0]; ppy = xs[1]; ppz = TWO_D ? 0.0f : xs[2];
                             prev_s = s;
                         }
                     }
