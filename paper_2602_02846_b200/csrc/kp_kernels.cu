@@ -2,21 +2,27 @@
 // plus reset/start/debug/trajectory helpers.
 //
 // One iteration (Alg. 1 lines 6-9) = three launches on one
-// stream, captured M iterations at a time into a CUDA graph:
+// stream, captured 8 iterations at a time into a CUDA graph with programmatic
+// dependent launch between the kernels:
 //
-//   k_propagate<MODEL>   Alg. 2.  One thread per V_U slot
-//                        (frontier position x branch).  Philox/SplitMix draw,
-//                        RK4 rollout streamed in registers with per-sample
-//                        validity against obstacles staged in shared memory,
-//                        path length, region, atomicMin on the encoded region
-//                        cost.  Admitted lanes write their slot record; a warp
-//                        ballot writes the admit / goal bitmask word.
+//   k_propagate<MODEL>   Alg. 2: per V_U slot (frontier
+//                        position x branch) a Philox/SplitMix draw, the
+//                        rollout (RK4 in registers; closed form for the double
+//                        integrator), per-sample validity against the
+//                        obstacles staged in shared memory, path length,
+//                        region, atomicMin on the encoded region cost;
+//                        admitted slots write their record and admit / goal
+//                        bit.  Two paths: step-sorted (a block sorts its chunk
+//                        by step count, a thread per slot; quadcopter rollouts
+//                        split in two passes with compaction) and, for the
+//                        double integrator's one-wave launches, sample-parallel
+//                        (flat_phase: a batch of items flattened into samples).
 //   k_select_reduce      Alg. 3 + the commit test of Alg. 4.
-//                        Element space = [live nodes, padded to 32] ++ [slots].
-//                        Live nodes: prune rules in SPEC.md:434-437 priority
-//                        order; slots: commit iff admitted and acc bits ==
-//                        region minimum.  Per-tile counts (keep, active,
-//                        commit); the last block scans the tile counts.
+//                        Element space = [live nodes] ++ [slots, or 32-slot
+//                        mask words when few are admitted].  Live nodes: prune
+//                        rules in SPEC.md:434-437 priority order; slots: commit
+//                        iff admitted and acc bits == region minimum.
+//                        Per-tile counts (keep, active, commit).
 //   k_select_scatter     Re-derives each element's flags, block scan + tile
 //                        prefix -> positions.  Survivors go to the next live /
 //                        frontier lists in id order; committed slots get node
@@ -28,7 +34,8 @@
 //                        timeline / TTFS from %globaltimer, termination.
 //
 // No kernel waits on another block: cross-block results flow through the
-// "last block" ticket pattern (threadfence + atomic counter), never a spin.
+// "last block" ticket pattern (acq_rel atomic counter), never a spin; the one
+// in-block wait is the split rollouts' second pass behind a block barrier.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cmath>
