@@ -566,9 +566,10 @@ def run_sweep(args, scenario):
     s["planner"]["max_slots"] = 1 << 22
     rows = []
     with ClockSampler(0) as clk, Planner(s, device=0, seed=1) as g:
-        g.sweep(1 << 10, launches=3)  # warm-up
+        g.sweep(1 << 10, launches=max(3, args.warmup))  # warm-up
         for k in range(14, 23):
             n = (1 << k) // int(s["planner"]["lambda"])
+            g.sweep(n, launches=max(3, args.warmup))  # untimed launches at this size
             ms, one = g.sweep(n, launches=max(3, args.steps))
             ops = (one["rk4_steps"] * OPS_PER_STEP[model] + one["items"] * OPS_PER_ITEM
                    + one["box_tests"] * OPS_PER_BOX + one["sphere_tests"] * OPS_PER_SPHERE
@@ -580,8 +581,8 @@ def run_sweep(args, scenario):
                          "frac": rate / pk["fp32_lane_ops"]})
     best = max(rows, key=lambda r: r["frac"])
     line = {"metric": "node propagations/sec (propagate kernel, synthetic frontier sweep)",
-            "value": best["items_per_s"], "unit": "propagations/s", "n_gpus": 1, "steps": args.steps,
-            "warmup": 1, "higher_is_better": True, "dtype": "f32", "data": "synthetic frontier (positions uniform "
+            "value": best["items_per_s"], "unit": "propagations/s", "n_gpus": 1, "steps": max(3, args.steps),
+            "warmup": max(3, args.warmup), "higher_is_better": True, "dtype": "f32", "data": "synthetic frontier (positions uniform "
             "in free space, hover-ish), region table reset per launch",
             "config": {"workload": f"{args.config} propagate sweep 2^14..2^22 samples per launch", "lambda":
                        s["planner"]["lambda"]},
