@@ -98,6 +98,12 @@ struct PropCfg {
 int prop_threads(int model) { return model == 3 ? PropCfg<3>::T : PropCfg<1>::T; }
 #define KP_SORT_BUCKETS 64
 
+// the split rollouts' per-group masks (32 entries) and the per-block scratch
+// (1024 slots) bound a chunk at 1024 slots in 32 groups
+static_assert(PropCfg<0>::T * PropCfg<0>::MAXG <= 1024 && PropCfg<1>::T * PropCfg<1>::MAXG <= 1024 &&
+                  PropCfg<2>::T * PropCfg<2>::MAXG <= 1024 && PropCfg<3>::T * PropCfg<3>::MAXG <= 1024,
+              "propagate chunks hold at most 1024 slots");
+
 template <int MODEL>
 struct PropSmem {
     float u[Model<MODEL>::M][PropCfg<MODEL>::T * PropCfg<MODEL>::MAXG];
