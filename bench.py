@@ -371,7 +371,7 @@ def run_b200(args, scenario):
         ttfs = [r["first_solution_s"] * 1e3 for r in results if r["found"]]
         costs = [r["best_cost"] for r in results if r["found"]]
         launches = prof1["kernel_launches"] - prof0["kernel_launches"] + 2 * len(seeds)
-        ctl_bytes = 98_632  # sizeof(KpCtl): the result block read back per query
+        ctl_bytes = 328 + 256 * 24  # result block read back per query: KpCtl header + 256 timeline entries (kp_capi.cpp fetch_ctl)
         line = {
             "metric": "node propagations/sec", "value": value, "unit": "propagations/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / len(seeds),

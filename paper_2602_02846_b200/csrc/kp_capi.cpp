@@ -16,6 +16,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -79,6 +80,7 @@ struct kp_planner {
     int sms = 148;
     int grid_prop = 0, grid_sel = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t fetch_stream = nullptr;  // result fetch that need not wait for trailing no-op launches
     cudaGraphExec_t graph = nullptr;
     uint32_t* host_done = nullptr;  // pinned, mapped
     std::vector<void*> allocs;
@@ -95,6 +97,7 @@ struct kp_planner {
     std::vector<float> boxes, spheres;  // host copies for start-state validation
     float* h_x0 = nullptr;              // pinned staging for the query's start state
     KpCtl* h_ctl = nullptr;             // pinned copy target for asynchronous result fetches
+    size_t last_fetch_bytes = 0;
 
     template <class T>
     T* dalloc(size_t count) {
@@ -113,6 +116,7 @@ struct kp_planner {
         if (h_x0) cudaFreeHost(h_x0);
         if (h_ctl) cudaFreeHost(h_ctl);
         if (stream) cudaStreamDestroy(stream);
+        if (fetch_stream) cudaStreamDestroy(fetch_stream);
     }
 };
 
@@ -474,9 +478,28 @@ void check_invariants() {
     if (code) throw KpError(KP_ERR_CUDA, "device invariant check " + std::to_string(code) + " failed");
 }
 
-void fetch_ctl(kp_planner* pl) {
-    cuda_check(cudaMemcpyAsync(&pl->ctl, pl->B.ctl, sizeof(KpCtl), cudaMemcpyDeviceToHost, pl->stream), "ctl D2H");
-    cuda_check(cudaStreamSynchronize(pl->stream), "ctl sync");
+// Result block D2H.  Default: ordered after everything queued on the
+// planner's stream.  after_done: the device has raised the done word, so the
+// control block is final (the boundary fences it before the mapped write) and
+// the trailing no-op launches of the graphs in flight never write it: read it
+// on a side stream instead of waiting for them.  Only the header and the
+// timeline entries in use are copied (pinned staging).
+void fetch_ctl(kp_planner* pl, bool after_done = false) {
+    constexpr size_t head = offsetof(KpCtl, timeline);
+    constexpr size_t win = 256;  // timeline entries in the first copy
+    cudaStream_t st = after_done ? pl->fetch_stream : pl->stream;
+    cuda_check(cudaMemcpyAsync(pl->h_ctl, pl->B.ctl, head + win * sizeof(KpTimeline), cudaMemcpyDeviceToHost, st),
+               "ctl D2H");
+    cuda_check(cudaStreamSynchronize(st), "ctl sync");
+    const size_t len = std::min<size_t>(pl->h_ctl->timeline_len, KP_TIMELINE_CAP);
+    if (len > win) {
+        cuda_check(cudaMemcpyAsync(pl->h_ctl->timeline + win, pl->B.ctl->timeline + win,
+                                   (len - win) * sizeof(KpTimeline), cudaMemcpyDeviceToHost, st),
+                   "ctl timeline D2H");
+        cuda_check(cudaStreamSynchronize(st), "ctl timeline sync");
+    }
+    std::memcpy(&pl->ctl, pl->h_ctl, head + std::max(len, win) * sizeof(KpTimeline));
+    pl->last_fetch_bytes = head + std::max(len, win) * sizeof(KpTimeline);
     pl->ctl_valid = true;
     check_invariants();
 }
@@ -590,6 +613,7 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         if (prop.major < 10) throw KpError(KP_ERR_CUDA, "device is not sm_100 class (built for sm_100a only)");
         pl->sms = prop.multiProcessorCount;
         cuda_check(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaStreamCreateWithFlags(&pl->fetch_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         void* hd = nullptr;
         cuda_check(cudaHostAlloc(&hd, 64, cudaHostAllocMapped), "cudaHostAlloc");
         pl->host_done = static_cast<uint32_t*>(hd);
@@ -822,7 +846,7 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
                 ++n_launched;
             }
         }
-        fetch_ctl(pl);
+        fetch_ctl(pl, /*after_done=*/!pl->profiling);
         if (pl->ctl.error == 8)
             throw KpError(KP_ERR_SLOT_OVERFLOW, "lambda*|V_A| exceeded max_slots; raise kp_config_desc.max_slots");
         fill_result(pl, out);
