@@ -117,12 +117,12 @@ struct PropSmem {
     uint32_t gbase[32];
     uint32_t n_surv, claim;
     uint32_t chunk;
-    unsigned long long cnt[6];
+    uint32_t cnt[6];
 };
 
 // Work counters of a propagate launch: warp-aggregated, then block-aggregated,
 // then one atomic per counter and block.
-KP_DEV void count_flush(KpCtl* ctl, uint32_t* c, unsigned long long* cnt, int lane) {
+KP_DEV void count_flush(KpCtl* ctl, uint32_t* c, uint32_t* cnt, int lane) {
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
 #pragma unroll
@@ -131,22 +131,22 @@ KP_DEV void count_flush(KpCtl* ctl, uint32_t* c, unsigned long long* cnt, int la
     if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < 6; ++k)
-            if (c[k]) atomicAdd(&cnt[k], static_cast<unsigned long long>(c[k]));
+            if (c[k]) atomicAdd(&cnt[k], c[k]);  // 32-bit: a native shared atomic
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         if (cnt[0]) {
-            atomicAdd(&ctl->stats.valid, cnt[0]);
-            atomicAdd(&ctl->n_valid_iter, static_cast<uint32_t>(cnt[0]));
+            atomicAdd(&ctl->stats.valid, static_cast<unsigned long long>(cnt[0]));
+            atomicAdd(&ctl->n_valid_iter, cnt[0]);
         }
         if (cnt[1]) {
-            atomicAdd(&ctl->stats.admitted, cnt[1]);
-            atomicAdd(&ctl->n_adm_iter, static_cast<uint32_t>(cnt[1]));
+            atomicAdd(&ctl->stats.admitted, static_cast<unsigned long long>(cnt[1]));
+            atomicAdd(&ctl->n_adm_iter, cnt[1]);
         }
-        if (cnt[2]) atomicAdd(&ctl->stats.rk4_steps, cnt[2]);
-        if (cnt[3]) atomicAdd(&ctl->stats.interp_points, cnt[3]);
-        if (cnt[4]) atomicAdd(&ctl->stats.box_tests, cnt[4]);
-        if (cnt[5]) atomicAdd(&ctl->stats.sphere_tests, cnt[5]);
+        if (cnt[2]) atomicAdd(&ctl->stats.rk4_steps, static_cast<unsigned long long>(cnt[2]));
+        if (cnt[3]) atomicAdd(&ctl->stats.interp_points, static_cast<unsigned long long>(cnt[3]));
+        if (cnt[4]) atomicAdd(&ctl->stats.box_tests, static_cast<unsigned long long>(cnt[4]));
+        if (cnt[5]) atomicAdd(&ctl->stats.sphere_tests, static_cast<unsigned long long>(cnt[5]));
     }
 }
 
@@ -383,7 +383,8 @@ KP_DEV bool check_sample(const KpProblem& P, const Env& E, const float* xs, floa
         for (int k = 0; k < N; ++k) ok = ok && isfinite(xs[k]);
     }
     const float nx = xs[0], ny = xs[1], nz = TWO_D ? 0.0f : xs[2];
-    const bool inb = within_bounds<MODEL>(P, xs);
+    // closed form with finite bounds: velocities were checked once per item (vel_ok_at_end)
+    const bool inb = within_bounds<MODEL>(P, xs, !(closed_form<MODEL>() && !P.check_finite));
     const bool hit = in_obstacle(P, E, nx, ny, nz, c[4], c[5]);
     ok = ok && inb && !hit;
     const float dx = nx - px, dy = ny - py, dz = nz - pz;
@@ -398,26 +399,28 @@ KP_DEV bool check_sample(const KpProblem& P, const Env& E, const float* xs, floa
 #ifndef KP_FLAT_ITEMS
 #define KP_FLAT_ITEMS 512u  // items per sample-parallel batch (a multiple of the block size)
 #endif
-#ifndef KP_IDX_STEP
-#define KP_IDX_STEP 8u      // samples per entry of the interleaved path's sample -> item index
+#ifndef KP_FLAT_K
+#define KP_FLAT_K 2u        // samples per chunk of the sample-parallel path
 #endif
 
 // Sample-parallel propagate for the double integrator (closed form, §4 of
 // DESIGN.md), used for one-wave launches (at most flat_nb items per block).
 // Its samples do not depend on one another, so a batch of items is flattened
-// into its samples and the whole block checks them: the batch takes about
-// (sum of step counts) / threads rounds instead of the longest item's step
-// count, which bounds a one-wave launch in the step-sorted path.  Per batch:
-// (1) one item per thread draws (u, dt), stages the parent state and counts
-// its samples; (2) block scan of the counts; (3) sample checks (bounds,
-// obstacles, interpolated points) and segment lengths, IL: interleaved over
-// the block (a warp's lanes on consecutive samples of a few items: coherent
-// obstacle lookups), else a contiguous run per thread (long rollouts); an
-// item with a failed sample is flagged and its remaining samples skipped;
-// segment lengths go into the item's fixed-point path length (order-
-// independent, §4); (4) the owner thread converts the length, computes region
-// and goal, and admits the candidate.
-template <int MODEL, bool IL>
+// into chunks of K consecutive samples and the whole block checks them: the
+// batch takes about (sum of chunk counts) / threads rounds instead of the
+// longest item's step count, which bounds a one-wave launch in the
+// step-sorted path.  Per batch: (1) one item per thread draws (u, dt), stages
+// the parent state, checks the velocity bounds once (vel_ok_at_end: an item
+// failing them gets no chunks) and counts its chunks; (2) block scan of the
+// counts; (3) chunks interleaved over the block: bounds, obstacles,
+// interpolated points and segment lengths of each sample; an item with a
+// failed sample is flagged and its remaining chunks skipped; each chunk adds
+// its fixed-point length to its item once (order-independent, §4); (4) the
+// owner thread converts the length, computes region and goal, and admits the
+// candidate.  K = 2 measured fastest (K = 4 and 8, one sample per thread
+// interleaved, and contiguous runs per thread were all slower: the shorter a
+// chunk, the less the lanes of a warp wait on each other's chunk tails).
+template <int MODEL>
 KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, unsigned char* dyn) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
@@ -425,9 +428,10 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
     constexpr uint32_t NWARP = T / 32;
     constexpr uint32_t IPT = (KP_FLAT_ITEMS + T - 1) / T;  // items per thread in a batch
     constexpr uint32_t FB = IPT * T;                        // items per batch (== P.flat_nb)
-    constexpr int RW = (N + M + 2 + 3) / 4;  // float4 words per item record: x0, u, dt, S
+    constexpr int RW = (N + M + 3 + 3) / 4;  // float4 words per item record: x0, u, dt, S, seff
     constexpr bool TWO_D = (MODEL == 0);
-    __shared__ unsigned long long fcnt[6];
+    constexpr uint32_t K = KP_FLAT_K;
+    __shared__ uint32_t fcnt[6];
     __shared__ uint32_t wsum[NWARP];
     __shared__ uint32_t fchunk;
     float4* const rec = reinterpret_cast<float4*>(dyn + P.flat_rec);
@@ -469,6 +473,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 node[k] = 0;
                 seffk[k] = 0;
                 acc_p[k] = 0.0f;
+                uint32_t vbad = 0u;
                 if (i < cend) {
                     const uint32_t f = i / lam;
                     const uint32_t br = i - f * lam;
@@ -486,17 +491,21 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                     const int S = step_count(P, dt);
                     // the shortened last step may be empty (dt - (S-1) h <= 0): then
                     // the rollout ends at sample S - 1 (as integrate_steps)
-                    seffk[k] = static_cast<uint32_t>((S > 1 && !(dt - static_cast<float>(S - 1) * P.h > 0.0f)) ? S - 1 : S);
+                    seffk[k] = static_cast<uint32_t>(effective_samples(P, dt, S));
+                    // velocity bounds once per item: an item failing them has no samples to check
+                    if (!P.check_finite && !vel_ok_at_end<MODEL>(P, r, u, dt, S, static_cast<int>(seffk[k]))) vbad = 1u;
 #pragma unroll
                     for (int d = 0; d < M; ++d) r[N + d] = u[d];
                     r[N + M] = dt;
                     r[N + M + 1] = __int_as_float(S);
+                    r[N + M + 2] = __int_as_float(static_cast<int>(seffk[k]));
 #pragma unroll
                     for (int w = 0; w < RW; ++w)
                         rec[p * RW + w] = make_float4(r[4 * w], r[4 * w + 1], r[4 * w + 2], r[4 * w + 3]);
                 }
-                seff += seffk[k];
-                bad[p] = 0u;
+                if (vbad) seffk[k] = 0;  // no samples: skipped by every mapping, dropped by the owner
+                seff += (seffk[k] + K - 1) / K;
+                bad[p] = vbad;
                 len_lo[p] = 0u;
                 len_hi[p] = 0u;
             }
@@ -525,32 +534,34 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
 #pragma unroll
                 for (uint32_t k = 0; k < IPT; ++k) {
                     off[threadIdx.x * IPT + k] = o;
-                    o += seffk[k];
+                    o += (seffk[k] + K - 1) / K;
                 }
                 if (threadIdx.x == T - 1) off[FB] = o;
             }
             __syncthreads();
-            if constexpr (IL) {
-                // (3) samples interleaved over the block: round r, thread t checks
-                // sample r*T + t, so a warp's lanes hold consecutive samples of a
-                // few items (nearby points: coherent broad / narrow phases)
+            {
+                // (3) chunks of K consecutive samples (one item each), interleaved
+                // over the block: round r, thread t takes chunk r*T + t, so every
+                // lane changes items at the same loop iteration (one convergent
+                // record load per K samples), a warp's lanes hold consecutive
+                // chunks of a few items (nearby points: coherent broad / narrow
+                // phases), and each chunk adds its length to its item once
                 const uint32_t U = off[FB];
-                uint16_t* const idx = reinterpret_cast<uint16_t*>(dyn + P.flat_idx);  // item of sample KP_IDX_STEP * k
+                uint16_t* const cidx = reinterpret_cast<uint16_t*>(dyn + P.flat_idx);  // item of each chunk
                 {
                     uint32_t o = excl;
 #pragma unroll
                     for (uint32_t k = 0; k < IPT; ++k) {
-                        for (uint32_t m = (o + KP_IDX_STEP - 1) / KP_IDX_STEP; m * KP_IDX_STEP < o + seffk[k]; ++m)
-                            idx[m] = static_cast<uint16_t>(threadIdx.x * IPT + k);
-                        o += seffk[k];
+                        const uint32_t nch = (seffk[k] + K - 1) / K;
+                        for (uint32_t j = 0; j < nch; ++j) cidx[o + j] = static_cast<uint16_t>(threadIdx.x * IPT + k);
+                        o += nch;
                     }
                 }
                 __syncthreads();
                 for (uint32_t q0 = 0; q0 < U; q0 += T) {
                     const uint32_t q = q0 + threadIdx.x;
                     if (q >= U) break;
-                    uint32_t pi = idx[q / KP_IDX_STEP];
-                    while (off[pi + 1] <= q) ++pi;
+                    const uint32_t pi = cidx[q];
                     if (bad[pi]) continue;
                     float x0[N], u[M];
                     float r[RW * 4];
@@ -565,93 +576,37 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                     for (int d = 0; d < M; ++d) u[d] = r[N + d];
                     const float dt = r[N + M];
                     const int S = __float_as_int(r[N + M + 1]);
-                    const int s = static_cast<int>(q - off[pi]) + 1;
-                    float xs[N], xp[N];
-                    di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
-                    if (s == 1) {
-#pragma unroll
-                        for (int d = 0; d < N; ++d) xp[d] = x0[d];
+                    const int se = __float_as_int(r[N + M + 2]);
+                    const int s0 = static_cast<int>(q - off[pi]) * static_cast<int>(K) + 1;
+                    const int s1 = min(se, s0 + static_cast<int>(K) - 1);
+                    float px, py, pz;
+                    if (s0 == 1) {
+                        px = x0[0]; py = x0[1]; pz = TWO_D ? 0.0f : x0[2];
                     } else {
-                        di_sample<MODEL>(x0, u, static_cast<float>(s - 1) * P.h, xp);
+                        float xp[N];
+                        di_sample<MODEL>(x0, u, static_cast<float>(s0 - 1) * P.h, xp);
+                        px = xp[0]; py = xp[1]; pz = TWO_D ? 0.0f : xp[2];
                     }
-                    const float px = xp[0], py = xp[1], pz = TWO_D ? 0.0f : xp[2];
-                    float d;
-                    if (!check_sample<MODEL>(P, E, xs, px, py, pz, d, c)) bad[pi] = 1u;
-                    const long long fx = len_fixed(d);
-                    atomicAdd(len_lo + pi, static_cast<uint32_t>(fx & 0xFFFFFF));
-                    atomicAdd(len_hi + pi, static_cast<uint32_t>(fx >> 24));
+                    long long run = 0;
+                    bool ok = true;
+                    for (int s = s0; s <= s1; ++s) {
+                        float xs[N];
+                        di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
+                        float d;
+                        if (!check_sample<MODEL>(P, E, xs, px, py, pz, d, c)) {
+                            ok = false;
+                            break;
+                        }
+                        run += len_fixed(d);
+                        px = xs[0]; py = xs[1]; pz = TWO_D ? 0.0f : xs[2];
+                    }
+                    if (!ok) {
+                        bad[pi] = 1u;
+                    } else if (run) {
+                        atomicAdd(len_lo + pi, static_cast<uint32_t>(run & 0xFFFFFF));
+                        atomicAdd(len_hi + pi, static_cast<uint32_t>(run >> 24));
+                    }
                 }
-            } else {
-                // (3) a contiguous run of samples per thread
-                const uint32_t U = off[FB];
-                const uint32_t qa = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x) * U) / T);
-                const uint32_t qb = static_cast<uint32_t>((static_cast<unsigned long long>(threadIdx.x + 1) * U) / T);
-                if (qa < qb) {
-                    uint32_t lo = 0, hi = FB;  // off[lo] <= qa < off[hi]
-                    while (hi - lo > 1) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (off[mid] <= qa) lo = mid;
-                        else hi = mid;
-                    }
-                    uint32_t pi = lo, pbeg = off[lo], pend = off[lo + 1];
-                    float x0[N], u[M], dt = 0.0f;
-                    int S = 0, prev_s = -1;
-                    float ppx = 0.0f, ppy = 0.0f, ppz = 0.0f;
-                    long long run = 0;  // fixed-point length of this thread's run of item pi
-                    auto flush = [&](uint32_t item) {
-                        if (run) {
-                            atomicAdd(len_lo + item, static_cast<uint32_t>(run & 0xFFFFFF));
-                            atomicAdd(len_hi + item, static_cast<uint32_t>(run >> 24));
-                        }
-                        run = 0;
-                    };
-                    for (uint32_t q = qa; q < qb; ++q) {
-                        if (q >= pend) {  // next item with samples (zero-sample items are skipped)
-                            flush(pi);
-                            do {
-                                ++pi;
-                                pbeg = pend;
-                                pend = off[pi + 1];
-                            } while (q >= pend);
-                            prev_s = -1;
-                        }
-                        {  // the item record, every sample: lanes change items at different samples
-                            float r[RW * 4];
-#pragma unroll
-                            for (int w = 0; w < RW; ++w) {
-                                const float4 v = rec[pi * RW + w];
-                                r[4 * w] = v.x; r[4 * w + 1] = v.y; r[4 * w + 2] = v.z; r[4 * w + 3] = v.w;
-                            }
-#pragma unroll
-                            for (int d = 0; d < N; ++d) x0[d] = r[d];
-#pragma unroll
-                            for (int d = 0; d < M; ++d) u[d] = r[N + d];
-                            dt = r[N + M];
-                            S = __float_as_int(r[N + M + 1]);
-                        }
-                        const int s = static_cast<int>(q - pbeg) + 1;  // sample index 1..seff
-                        if (!bad[pi]) {
-                            float xs[N];
-                            di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
-                            float px, py, pz;
-                            if (s == 1) {
-                                px = x0[0]; py = x0[1]; pz = TWO_D ? 0.0f : x0[2];
-                            } else if (prev_s == s - 1) {
-                                px = ppx; py = ppy; pz = ppz;
-                            } else {
-                                float xp[N];
-                                di_sample<MODEL>(x0, u, static_cast<float>(s - 1) * P.h, xp);
-                                px = xp[0]; py = xp[1]; pz = TWO_D ? 0.0f : xp[2];
-                            }
-                            float d;
-                            if (!check_sample<MODEL>(P, E, xs, px, py, pz, d, c)) bad[pi] = 1u;
-                            run += len_fixed(d);
-                            ppx = xs[0]; ppy = xs[1]; ppz = TWO_D ? 0.0f : xs[2];
-                            prev_s = s;
-                        }
-                    }
-                    flush(pi);
-            }
             }
             __syncthreads();
             // (4) owner thread: path length, region, admission
@@ -714,8 +669,7 @@ __global__ void __launch_bounds__(PropCfg<MODEL>::T, PropCfg<MODEL>::MIN_BLOCKS)
         // small launches are latency-bound: flatten them into samples; large
         // ones are issue-bound, where the step-sorted path runs fewer instructions
         if (P.flat_on && B.ctl->n_items <= P.flat_max) {
-            if (P.flat_il) flat_phase<MODEL, true>(P, B, E, dyn);
-            else flat_phase<MODEL, false>(P, B, E, dyn);
+            flat_phase<MODEL>(P, B, E, dyn);
             return;
         }
     }
@@ -1486,11 +1440,12 @@ void plan_propagate_smem(KpProblem& P) {
     const char* env = std::getenv("KP_FLAT");
     if ((P.model == 0 || P.model == 1) && !(env && env[0] == '0')) {
         const uint32_t nb = (KP_FLAT_ITEMS + T - 1) / T * T;
-        const uint32_t rw = static_cast<uint32_t>((P.n + P.m + 2 + 3) / 4);
+        const uint32_t rw = static_cast<uint32_t>((P.n + P.m + 3 + 3) / 4);
         const size_t rec = pad16(static_cast<size_t>(nb) * rw * 16);
         const size_t offs = pad16((nb + 1) * 4ull), badb = pad16(nb * 4ull), lenb = pad16(2 * nb * 4ull);
         const uint32_t smax = static_cast<uint32_t>(std::ceil(static_cast<double>(P.t_prop) / P.h)) + 1u;
-        const size_t idxb = pad16((static_cast<size_t>(nb) * smax / KP_IDX_STEP + 2) * 2);
+        // chunk -> item index
+        const size_t idxb = pad16(static_cast<size_t>(nb) * ((smax + KP_FLAT_K - 1) / KP_FLAT_K) * 2);
         const size_t flat = rec + offs + badb + lenb + idxb;
         if (base + flat <= 96 * 1024) {
             P.flat_on = 1;
@@ -1500,13 +1455,6 @@ void plan_propagate_smem(KpProblem& P) {
             P.flat_bad = static_cast<uint32_t>(base + rec + offs);
             P.flat_len = static_cast<uint32_t>(base + rec + offs + badb);
             P.flat_idx = static_cast<uint32_t>(base + rec + offs + badb + lenb);
-            // sample-to-thread mapping: interleaved (a warp's lanes on consecutive
-            // samples of a few items: coherent obstacle lookups) for rollouts of
-            // up to 32 samples; contiguous runs per thread (previous sample
-            // carried, one record load and one length update per run) for longer
-            // ones, where they measured faster (profiles/README.md)
-            const char* il = std::getenv("KP_FLAT_IL");
-            P.flat_il = il ? (il[0] != '0') : (smax <= 32 ? 1 : 0);
             area = std::max(area, flat);
         }
     }

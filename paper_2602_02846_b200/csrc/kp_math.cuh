@@ -348,10 +348,12 @@ KP_DEV bool in_obstacle(const KpProblem& P, const Env& E, float px, float py, fl
 }
 
 // is_state_valid minus the obstacle part, which the caller
-// does on the (px, py, pz) projection.
+// does on the (px, py, pz) projection.  vel = false skips the velocity dims of
+// a closed-form model (checked once per item instead, vel_ok_at_end).
 template <int MODEL>
-KP_DEV bool within_bounds(const KpProblem& P, const float* x) {
+KP_DEV bool within_bounds(const KpProblem& P, const float* x, bool vel = true) {
     constexpr int N = Model<MODEL>::N;
+    constexpr int D = closed_form<MODEL>() ? N / 2 : N;  // dims checked at every sample when !vel
     // state bounds with the workspace bounds folded into the
     // position dims on the host: x >= max(lo_s, lo_w) <=> x >= lo_s && x >= lo_w.
     // Three independent compare chains (the predicate-accumulating FSETP form
@@ -359,6 +361,7 @@ KP_DEV bool within_bounds(const KpProblem& P, const float* x) {
     bool ok0 = true, ok1 = true, ok2 = true;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
+        if (i >= D && !vel) break;
         const bool in = (x[i] >= P.blo[i]) & (x[i] <= P.bhi[i]);
         if (i % 3 == 0) ok0 = ok0 & in;
         else if (i % 3 == 1) ok1 = ok1 & in;
@@ -484,6 +487,33 @@ KP_DEV int advance(const KpProblem& P, const float* x0, float* x, const float* u
     }
 }
 
+// Closed-form models, velocity bounds once per item: v(t) = fma(u, t, v0) is
+// monotone in t (fma is correctly rounded, hence monotone) and the sample
+// times 0 < h < 2h < ... < t_last increase (t_last = dt when the last step is
+// non-empty, dt > fl((S-1) h)), so with a valid parent (samples[0] is a stored
+// node) every sample's velocity lies inside its interval bounds iff the last
+// sample's does.  The per-sample checks then cover the position dims only;
+// the verdict is the same as checking every sample.  Only
+// for finite bounds (P.check_finite == 0), where no sample can diverge.
+template <int MODEL>
+KP_DEV bool vel_ok_at_end(const KpProblem& P, const float* x0, const float* u, float dt, int S, int seff) {
+    constexpr int D = Model<MODEL>::N / 2;
+    const float t = (seff == S) ? dt : static_cast<float>(seff) * P.h;
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const float v = fmaf(u[i], t, x0[D + i]);
+        ok = ok & (v >= P.blo[D + i]) & (v <= P.bhi[D + i]);
+    }
+    return ok;
+}
+
+// Samples of a rollout with S steps: S, or S - 1 when the shortened last step
+// is empty (dt - (S-1) h <= 0).
+KP_DEV int effective_samples(const KpProblem& P, float dt, int S) {
+    return (S > 1 && !(dt - static_cast<float>(S - 1) * P.h > 0.0f)) ? S - 1 : S;
+}
+
 template <int MODEL>
 KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const float* u, float dt, int S, int s0, int s1,
                            float& total, ItemOut& o) {
@@ -495,6 +525,13 @@ KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const flo
 #pragma unroll
     for (int i = 0; i < N; ++i) x0[i] = x[i];
     long long fx = 0;  // closed form: fixed-point path length
+    bool vel = true;   // check the velocity dims at every sample
+    if constexpr (closed_form<MODEL>()) {
+        if (!P.check_finite) {
+            if (!vel_ok_at_end<MODEL>(P, x0, u, dt, S, effective_samples(P, dt, S))) return 1;
+            vel = false;
+        }
+    }
     for (int s = s0; s < s1; ++s) {
         const int st = advance<MODEL>(P, x0, x, u, dt, S, s, h6);
         if (st == 1) break;
@@ -503,7 +540,7 @@ KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const flo
         const float nx = x[0], ny = x[1], nz = TWO_D ? 0.0f : x[2];
         // bounds and obstacle test without a branch in between (one exit per step;
         // the broad-phase cell index is clamped, so out-of-bounds states are safe)
-        const bool inb = within_bounds<MODEL>(P, x);
+        const bool inb = within_bounds<MODEL>(P, x, vel);
         const bool hit = in_obstacle(P, E, nx, ny, nz, o.nbox, o.nsph);
         if (!inb || hit) return 1;
         const float dx = nx - px, dy = ny - py, dz = nz - pz;

@@ -90,7 +90,6 @@ struct KpProblem {
     int32_t flat_on;
     uint32_t flat_max;         // launches of at most this many items take the sample-parallel path
     uint32_t flat_nb;          // items per batch
-    int32_t flat_il;           // 1: samples interleaved over the block, 0: contiguous runs per thread
     uint32_t flat_rec, flat_offs, flat_bad, flat_len, flat_idx;
 };
 

@@ -220,22 +220,21 @@ def test_whole_run_bit_identical_steady_state(scene, iters):
         _compare_runs(g, o, rg, ro)
 
 
-@pytest.mark.parametrize("mode", ["interleaved", "runs", "step_sorted"])
+@pytest.mark.parametrize("mode", ["sample_parallel", "step_sorted"])
 @pytest.mark.parametrize("scene,iters", [("forest_di6", 24), ("zigzag2d", 40), ("building6d", 20)])
 def test_whole_run_bit_identical_propagate_paths(scene, iters, mode, monkeypatch):
-    """The double integrator's propagate paths (kp_kernels.cu flat_phase with
-    interleaved samples or contiguous runs per thread for one-wave launches,
+    """The double integrator's propagate paths (kp_kernels.cu flat_phase, the
+    sample-parallel path for one-wave launches,
     the step-sorted path for larger ones) each reproduce the restatement on
     their own: forced for every launch size here."""
     if mode == "step_sorted":
         monkeypatch.setenv("KP_FLAT", "0")
     else:
         monkeypatch.setenv("KP_FLAT_MAX", str(1 << 30))
-        monkeypatch.setenv("KP_FLAT_IL", "1" if mode == "interleaved" else "0")
     s = scenarios.load(scene)
     with Planner(s, seed=21) as g:
         rg = g.solve(budget_s=0.0, max_iterations=iters)
-    for k in ("KP_FLAT_MAX", "KP_FLAT", "KP_FLAT_IL"):
+    for k in ("KP_FLAT_MAX", "KP_FLAT"):
         monkeypatch.delenv(k, raising=False)
     o = kpo.Oracle(s, kpo.MIRROR32, seed=21, workers=8)
     ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
@@ -244,21 +243,20 @@ def test_whole_run_bit_identical_propagate_paths(scene, iters, mode, monkeypatch
 
 
 @pytest.mark.parametrize("t_prop,h,lam", [(0.02, 0.02, 32), (2.0, 0.02, 4), (0.5, 0.02, 1)])
-@pytest.mark.parametrize("mode", ["interleaved", "runs", "step_sorted"])
+@pytest.mark.parametrize("mode", ["sample_parallel", "step_sorted"])
 def test_whole_run_bit_identical_rollout_lengths(t_prop, h, lam, mode, monkeypatch):
     """Rollout-length extremes on the double integrator's propagate paths: one
-    sample per rollout (t_prop = h), up to 101 samples (past the interleaved
-    path's 32-sample default and the step-count sort's 64 buckets), lambda = 1."""
+    sample per rollout (t_prop = h), up to 101 samples (past the step-count
+    sort's 64 buckets), lambda = 1."""
     if mode == "step_sorted":
         monkeypatch.setenv("KP_FLAT", "0")
     else:
         monkeypatch.setenv("KP_FLAT_MAX", str(1 << 30))
-        monkeypatch.setenv("KP_FLAT_IL", "1" if mode == "interleaved" else "0")
     s = scenarios.load("forest_di6", t_prop=t_prop, ode_step=h, collision_step=0.05, **{"lambda": lam})
     iters = 12
     with Planner(s, seed=3) as g:
         rg = g.solve(budget_s=0.0, max_iterations=iters)
-    for k in ("KP_FLAT_MAX", "KP_FLAT", "KP_FLAT_IL"):
+    for k in ("KP_FLAT_MAX", "KP_FLAT"):
         monkeypatch.delenv(k, raising=False)
     o = kpo.Oracle(s, kpo.MIRROR32, seed=3, workers=8)
     ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
