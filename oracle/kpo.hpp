@@ -426,19 +426,24 @@ bool propagate_ode(const ProblemDef& pd, const Consts<P>& k, const Vec<typename 
         const R hk = (s + 1 < S) ? h : dt - R(S - 1) * h;
         if (!(hk > R(0))) break;
         const R half = R(0.5) * hk;
-        derivative<P>(pd, k, x, u, k1);
-        for (int i = 0; i < n; ++i) t[i] = P::madd(half, k1[i], x[i]);
+        // slopes accumulated in production order: acc = ((k1 + 2 k2) + 2 k3) + k4
+        // (the device keeps only acc and the current stage live)
+        Vec<R>& acc = k1;
+        derivative<P>(pd, k, x, u, acc);
+        for (int i = 0; i < n; ++i) t[i] = P::madd(half, acc[i], x[i]);
         derivative<P>(pd, k, t, u, k2);
-        for (int i = 0; i < n; ++i) t[i] = P::madd(half, k2[i], x[i]);
+        for (int i = 0; i < n; ++i) {
+            t[i] = P::madd(half, k2[i], x[i]);
+            acc[i] = P::madd(R(2), k2[i], acc[i]);
+        }
         derivative<P>(pd, k, t, u, k3);
-        for (int i = 0; i < n; ++i) t[i] = P::madd(hk, k3[i], x[i]);
+        for (int i = 0; i < n; ++i) {
+            t[i] = P::madd(hk, k3[i], x[i]);
+            acc[i] = P::madd(R(2), k3[i], acc[i]);
+        }
         derivative<P>(pd, k, t, u, k4);
         const R sixth = hk / R(6);
-        for (int i = 0; i < n; ++i) {
-            const R a = k1[i] + k4[i];
-            const R b = k2[i] + k3[i];
-            x[i] = P::madd(sixth, P::madd(R(2), b, a), x[i]);
-        }
+        for (int i = 0; i < n; ++i) x[i] = P::madd(sixth, acc[i] + k4[i], x[i]);
         for (int ad : pd.angle_dims) x[ad] = wrap_angle<P>(x[ad]);
         for (int i = 0; i < n; ++i)
             if (!std::isfinite(x[i])) return false;

@@ -81,7 +81,10 @@ template <int MODEL>
 struct PropCfg {
     static constexpr int T = MODEL == 3 ? 256 : 512;  // threads per block
     static constexpr int MAXG = 1024 / T;             // slot rounds per chunk
-    static constexpr int MIN_BLOCKS = MODEL == 3 ? 3 : 2;
+#ifndef KP_QUAD_MINB
+#define KP_QUAD_MINB 3
+#endif
+    static constexpr int MIN_BLOCKS = MODEL == 3 ? KP_QUAD_MINB : 2;
     // Steps of the first pass of a split rollout (0: never split).  Only the
     // quadcopter splits: ~55 % of its items stop early (invalid), and a first
     // pass of 8 steps cuts its warp-steps by ~22 % (scripts/split_sim.py); for

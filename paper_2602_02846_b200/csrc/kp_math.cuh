@@ -103,7 +103,35 @@ KP_DEV void sample_item(const KpProblem& P, uint64_t seed, uint32_t it, uint32_t
 
 // ----------------------------------------------------------------- math ---
 // Pinned sincos recipe, identical to the oracle's.
+KP_DEV void sincos_poly(float r, float& s, float& c) {  // |r| <= pi/4
+    const float r2 = r * r;
+    float ps = fmaf(r2, 0x1.71de3ap-19f, -0x1.a01a02p-13f);
+    ps = fmaf(r2, ps, 0x1.111112p-7f);
+    ps = fmaf(r2, ps, -0x1.555556p-3f);
+    s = fmaf(r * r2, ps, r);
+    float pc = fmaf(r2, -0x1.27e4fcp-22f, 0x1.a01a02p-16f);
+    pc = fmaf(r2, pc, -0x1.6c16c2p-10f);
+    pc = fmaf(r2, pc, 0x1.555556p-5f);
+    pc = fmaf(r2, pc, -0.5f);
+    c = fmaf(r2, pc, 1.0f);
+}
+
+// SMALL: an angle whose state bounds keep it inside (-pi/4, pi/4) (the
+// quadcopter's roll and pitch, |phi|, |theta| <= 0.6; the airplane's flight
+// path angle, |gamma| <= 0.5).  When |x * 2/pi| < 1/2 for every active lane,
+// j = 0, r == x exactly (fma(-0, c, x) == x) and there is no quadrant fix-up:
+// the same bits as the general path without its reduction and select
+// instructions.  The test is a warp vote so the branch never diverges (a
+// divergent branch runs both paths); headings (psi) always take the general
+// path.
+template <bool SMALL = false>
 KP_DEV void sincos_recipe(float x, float& s_out, float& c_out) {
+    if constexpr (SMALL) {
+        if (fabsf(x * 0x1.45f306p-1f) < 0.5f) {
+            sincos_poly(x, s_out, c_out);
+            return;
+        }
+    }
     // j = rint(x * 2/pi) with round-half-even via the 1.5 * 2^23 magic add (bit-identical
     // to rintf for |x * 2/pi| < 2^22) and the quadrant from the sum's integer bits: no
     // XU-pipe conversion instructions
@@ -112,16 +140,8 @@ KP_DEV void sincos_recipe(float x, float& s_out, float& c_out) {
     const int q = __float_as_int(t) - 0x4B400000;
     float r = fmaf(-j, 0x1.921fb4p+0f, x);
     r = fmaf(-j, 0x1.4442d2p-24f, r);
-    const float r2 = r * r;
-    float ps = fmaf(r2, 0x1.71de3ap-19f, -0x1.a01a02p-13f);
-    ps = fmaf(r2, ps, 0x1.111112p-7f);
-    ps = fmaf(r2, ps, -0x1.555556p-3f);
-    const float s = fmaf(r * r2, ps, r);
-    float pc = fmaf(r2, -0x1.27e4fcp-22f, 0x1.a01a02p-16f);
-    pc = fmaf(r2, pc, -0x1.6c16c2p-10f);
-    pc = fmaf(r2, pc, 0x1.555556p-5f);
-    pc = fmaf(r2, pc, -0.5f);
-    const float c = fmaf(r2, pc, 1.0f);
+    float s, c;
+    sincos_poly(r, s, c);
     // quadrant select without branches: q&1 swaps (s, c) -> (c, -s); q&2 negates both
     float so = (q & 1) ? c : s;
     float co = (q & 1) ? -s : c;
@@ -142,6 +162,21 @@ KP_DEV float wrap_angle(float a) {
     return a;
 }
 
+// Two small-range angles at once (the quadcopter's roll and pitch): one branch
+// for both — the fast path when both have j = 0, else the general path for
+// both (same bits either way).
+KP_DEV void sincos2_small(float a, float b, float& sa, float& ca, float& sb, float& cb) {
+#ifndef KP_NO_SINCOS_FAST
+    if (fmaxf(fabsf(a * 0x1.45f306p-1f), fabsf(b * 0x1.45f306p-1f)) < 0.5f) {
+        sincos_poly(a, sa, ca);
+        sincos_poly(b, sb, cb);
+        return;
+    }
+#endif
+    sincos_recipe(a, sa, ca);
+    sincos_recipe(b, sb, cb);
+}
+
 // ------------------------------------------------------------ dynamics ----
 template <int MODEL> struct Model;
 template <> struct Model<0> { static constexpr int N = 4, M = 2, NA = 0, A0 = 0; };   // double_integrator_4d
@@ -159,14 +194,13 @@ KP_DEV void derivative(const KpProblem& P, const float* x, const float* u, float
     } else if constexpr (MODEL == 2) {
         float sp, cp, sg, cg;
         sincos_recipe(x[3], sp, cp);
-        sincos_recipe(x[4], sg, cg);
+        sincos_recipe<true>(x[4], sg, cg);
         const float vc = x[5] * cg;
         f[0] = vc * cp; f[1] = vc * sp; f[2] = x[5] * sg;
         f[3] = u[0]; f[4] = u[1]; f[5] = u[2];
     } else {
         float sph, cph, sth, cth, sps, cps;
-        sincos_recipe(x[6], sph, cph);
-        sincos_recipe(x[7], sth, cth);
+        sincos2_small(x[6], x[7], sph, cph, sth, cth);
         sincos_recipe(x[8], sps, cps);
         const float a = u[0] * P.inv_m;
         const float t1 = cph * sth;
@@ -192,26 +226,41 @@ KP_DEV void derivative(const KpProblem& P, const float* x, const float* u, float
 template <int MODEL>
 KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk, float sixth) {
     constexpr int N = Model<MODEL>::N;
-    float k1[N], k2[N], k3[N], k4[N], t[N];
+    // the stage slopes are accumulated as they are produced, acc = k1 + 2 k2 +
+    // 2 k3 + k4 in that order: only acc and the current stage stay live (the
+    // quadcopter's 12-dim step otherwise holds k1 and k2 across later stages)
+    float k[N], acc[N], t[N];
     const float half = 0.5f * hk;
-    derivative<MODEL>(P, x, u, k1);
+    derivative<MODEL>(P, x, u, acc);
 #pragma unroll
-    for (int i = 0; i < N; ++i) t[i] = fmaf(half, k1[i], x[i]);
-    derivative<MODEL>(P, t, u, k2);
-#pragma unroll
-    for (int i = 0; i < N; ++i) t[i] = fmaf(half, k2[i], x[i]);
-    derivative<MODEL>(P, t, u, k3);
-#pragma unroll
-    for (int i = 0; i < N; ++i) t[i] = fmaf(hk, k3[i], x[i]);
-    derivative<MODEL>(P, t, u, k4);
+    for (int i = 0; i < N; ++i) t[i] = fmaf(half, acc[i], x[i]);
+    derivative<MODEL>(P, t, u, k);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-        const float a = k1[i] + k4[i];
-        const float b = k2[i] + k3[i];
-        x[i] = fmaf(sixth, fmaf(2.0f, b, a), x[i]);
+        t[i] = fmaf(half, k[i], x[i]);
+        acc[i] = fmaf(2.0f, k[i], acc[i]);
     }
+    derivative<MODEL>(P, t, u, k);
 #pragma unroll
-    for (int i = 0; i < Model<MODEL>::NA; ++i) x[Model<MODEL>::A0 + i] = wrap_angle(x[Model<MODEL>::A0 + i]);
+    for (int i = 0; i < N; ++i) {
+        t[i] = fmaf(hk, k[i], x[i]);
+        acc[i] = fmaf(2.0f, k[i], acc[i]);
+    }
+    derivative<MODEL>(P, t, u, k);
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = fmaf(sixth, acc[i] + k[i], x[i]);
+    if constexpr (Model<MODEL>::NA > 0) {
+        // one test for every angle: wrap_angle only changes |a| >= pi (and
+        // leaves pi itself and NaN unchanged), so wrapping all of them when
+        // any is out of range gives the same bits as testing each
+        float m = fabsf(x[Model<MODEL>::A0]);
+#pragma unroll
+        for (int i = 1; i < Model<MODEL>::NA; ++i) m = fmaxf(m, fabsf(x[Model<MODEL>::A0 + i]));
+        if (m >= 3.14159265358979323846f) {
+#pragma unroll
+            for (int i = 0; i < Model<MODEL>::NA; ++i) x[Model<MODEL>::A0 + i] = wrap_angle(x[Model<MODEL>::A0 + i]);
+        }
+    }
     if (!P.check_finite) return true;  // finite bounds reject inf / NaN in within_bounds anyway
     bool ok = true;
 #pragma unroll
