@@ -220,7 +220,9 @@ void build_problem(const kp_problem_desc* p, const kp_config_desc* c, KpProblem&
     if (p->goal_n_dims < 1 || p->goal_n_dims > KP_MAX_N) throw KpError(KP_ERR_SCHEMA, "bad goal dimensions");
     if (!(p->goal_radius > 0)) throw KpError(KP_ERR_SCHEMA, "goal radius must be > 0");
     P.goal_n = p->goal_n_dims;
+    P.goal_ident = 1;
     for (int i = 0; i < p->goal_n_dims; ++i) {
+        if (p->goal_dims[i] != i) P.goal_ident = 0;
         const int d = p->goal_dims[i];
         if (d < 0 || d >= n) throw KpError(KP_ERR_SCHEMA, "goal dimension out of range");
         if (!(p->goal_center[i] >= p->state_lo[d] && p->goal_center[i] <= p->state_hi[d]))
@@ -262,8 +264,10 @@ void build_problem(const kp_problem_desc* p, const kp_config_desc* c, KpProblem&
         throw KpError(KP_ERR_GRID_TOO_FINE, "region grid would have " + std::to_string(static_cast<double>(total)) +
                                                 " cells, above the ceiling " + std::to_string(ceiling));
     uint32_t stride = 1;
+    P.grid_ident = 1;
     for (int j = 0; j < P.grid_n; ++j) {
         const int d = p->grid_dims[j];
+        if (d != j) P.grid_ident = 0;
         P.grid_dims[j] = d;
         P.g_lo[j] = static_cast<float>(p->state_lo[d]);
         P.g_cells[j] = static_cast<int32_t>(cells[j]);

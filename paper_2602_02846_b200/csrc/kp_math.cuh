@@ -428,14 +428,17 @@ KP_DEV float pick(const float* x, int d) {
     return v;
 }
 
-// region_index.
-template <int N>
-KP_DEV uint32_t region_index(const KpProblem& P, const float* x) {
+// region_index.  IDENT: the decomposed dims are 0, 1, ...
+// (every bundled scene): the coordinates are read directly instead of through
+// the runtime-dimension select chain.
+template <int N, bool IDENT>
+KP_DEV uint32_t region_index_dims(const KpProblem& P, const float* x) {
     uint32_t r = 0;
 #pragma unroll
     for (int j = 0; j < KP_MAX_GRID; ++j) {
-        if (j >= P.grid_n) break;
-        const float v = (pick<N>(x, P.grid_dims[j]) - P.g_lo[j]) / P.g_side[j];
+        if (j >= P.grid_n || (IDENT && j >= N)) break;
+        const float xv = IDENT ? x[j < N ? j : 0] : pick<N>(x, P.grid_dims[j]);
+        const float v = (xv - P.g_lo[j]) / P.g_side[j];
         const float fv = floorf(v);
         uint32_t i;
         if (fv < 0.0f) i = 0;
@@ -446,18 +449,28 @@ KP_DEV uint32_t region_index(const KpProblem& P, const float* x) {
     return r;
 }
 
-// in_goal (cost.hpp:77-84), boundary inclusive.
 template <int N>
-KP_DEV bool in_goal(const KpProblem& P, const float* x) {
-    float d = pick<N>(x, P.goal_dims[0]) - P.goal_c[0];
+KP_DEV uint32_t region_index(const KpProblem& P, const float* x) {
+    return P.grid_ident ? region_index_dims<N, true>(P, x) : region_index_dims<N, false>(P, x);
+}
+
+// in_goal (cost.hpp:77-84), boundary inclusive.  IDENT as region_index.
+template <int N, bool IDENT>
+KP_DEV bool in_goal_dims(const KpProblem& P, const float* x) {
+    float d = (IDENT ? x[0] : pick<N>(x, P.goal_dims[0])) - P.goal_c[0];
     float d2 = d * d;
 #pragma unroll
     for (int i = 1; i < N; ++i) {
         if (i >= P.goal_n) break;
-        d = pick<N>(x, P.goal_dims[i]) - P.goal_c[i];
+        d = (IDENT ? x[i] : pick<N>(x, P.goal_dims[i])) - P.goal_c[i];
         d2 = fmaf(d, d, d2);
     }
     return d2 <= P.goal_r2;
+}
+
+template <int N>
+KP_DEV bool in_goal(const KpProblem& P, const float* x) {
+    return P.goal_ident ? in_goal_dims<N, true>(P, x) : in_goal_dims<N, false>(P, x);
 }
 
 // --------------------------------------------------------- work item ------

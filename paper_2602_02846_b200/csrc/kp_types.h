@@ -44,6 +44,7 @@ struct KpProblem {
     int32_t n_angle;
     int32_t angle_dims[3];
     int32_t goal_n;
+    int32_t goal_ident;      // goal_dims[i] == i for every i (read coordinates directly)
     int32_t goal_dims[KP_MAX_N];
     float goal_c[KP_MAX_N];
     float goal_r2;
@@ -56,6 +57,7 @@ struct KpProblem {
     double clo_d[KP_MAX_M], chi_d[KP_MAX_M];
     float wlo[3], whi[3];
     int32_t grid_n;
+    int32_t grid_ident;      // grid_dims[j] == j for every j
     int32_t grid_dims[KP_MAX_GRID];
     float g_lo[KP_MAX_GRID], g_side[KP_MAX_GRID];
     int32_t g_cells[KP_MAX_GRID];

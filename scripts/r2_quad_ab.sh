@@ -7,7 +7,7 @@ for f in abtmp/lib_*.so; do
   echo "== $(basename $f .so)" >> $OUT/ab.log
   for k in 20 22; do timeout 120 python scripts/prof_sweep.py building_quad12 $k >> $OUT/ab.log 2>&1; done
   timeout 120 python scripts/prof_sweep.py narrow_dubins6 22 >> $OUT/ab.log 2>&1
-  timeout 300 python scripts/ab_perf.py building_quad12 narrow_dubins6 >> $OUT/ab.log 2>&1
+  timeout 300 python scripts/ab_perf.py building_quad12 narrow_dubins6 forest_di6 >> $OUT/ab.log 2>&1
 done
 cp /tmp/lib_cur.so $L
 echo done
