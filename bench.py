@@ -82,6 +82,7 @@ class ClockSampler:
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.rows = []
+        self.stamps = []
         self.proc = None
 
     def __enter__(self):
@@ -101,6 +102,13 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
+            self.stamps.append(time.time())
+
+    def only_within(self, windows):
+        """Keep the samples taken inside the given (t0, t1) wall-clock windows."""
+        keep = [i for i, t in enumerate(self.stamps) if any(a <= t <= b for a, b in windows)]
+        self.rows = [self.rows[i] for i in keep]
+        self.stamps = [self.stamps[i] for i in keep]
 
     def __exit__(self, *exc):
         if self.proc:
@@ -565,12 +573,17 @@ def run_sweep(args, scenario):
     s["planner"]["capacity"] = max(int(s["planner"].get("capacity", 0)), (1 << 22) // 32)
     s["planner"]["max_slots"] = 1 << 22
     rows = []
+    windows = []  # clocks are kept from the timed launches only (the synthetic frontier is built on the host)
     with ClockSampler(0) as clk, Planner(s, device=0, seed=1) as g:
         g.sweep(1 << 10, launches=max(3, args.warmup))  # warm-up
         for k in range(14, 23):
             n = (1 << k) // int(s["planner"]["lambda"])
-            g.sweep(n, launches=max(3, args.warmup))  # untimed launches at this size
-            ms, one = g.sweep(n, launches=max(3, args.steps))
+            ms_w, _ = g.sweep(n, launches=max(3, args.warmup))  # untimed launches at this size
+            # at least ~0.25 s of launches per size, so the clock sampler sees the load
+            launches = max(3, args.steps, int(250.0 / max(ms_w, 1e-3)))
+            t0 = time.time()
+            ms, one = g.sweep(n, launches=launches)
+            windows.append((t0, time.time()))
             ops = (one["rk4_steps"] * OPS_PER_STEP[model] + one["items"] * OPS_PER_ITEM
                    + one["box_tests"] * OPS_PER_BOX + one["sphere_tests"] * OPS_PER_SPHERE
                    + one["interp_points"] * OPS_PER_INTERP)
@@ -578,7 +591,8 @@ def run_sweep(args, scenario):
             rows.append({"k": k, "items": one["items"], "frontier_nodes": n, "ms_per_launch": ms,
                          "items_per_s": one["items"] / (ms * 1e-3), "rk4_steps": one["rk4_steps"],
                          "lane_ops_per_launch": ops, "achieved_T_lane_ops": rate / 1e12,
-                         "frac": rate / pk["fp32_lane_ops"]})
+                         "frac": rate / pk["fp32_lane_ops"], "launches": launches})
+    clk.only_within(windows)
     best = max(rows, key=lambda r: r["frac"])
     line = {"metric": "node propagations/sec (propagate kernel, synthetic frontier sweep)",
             "value": best["items_per_s"], "unit": "propagations/s", "n_gpus": 1, "steps": max(3, args.steps),

@@ -287,6 +287,9 @@ void build_problem(const kp_problem_desc* p, const kp_config_desc* c, KpProblem&
     if (!(c->collision_step > 0)) throw KpError(KP_ERR_CONFIG, "collision_step must be > 0");
     if (c->rng_kind != KP_RNG_PHILOX && c->rng_kind != KP_RNG_SPLITMIX) throw KpError(KP_ERR_CONFIG, "unknown rng kind");
     P.lambda = c->lambda;
+    P.lam_shift = -1;
+    for (int b = 0; b < 31; ++b)
+        if (c->lambda == (1 << b)) P.lam_shift = b;
     P.i_max = c->i_max;
     P.rng_kind = c->rng_kind;
     P.deact = c->deactivate_after_expansion ? 1 : 0;

@@ -123,14 +123,11 @@ struct PropSmem {
     uint32_t cnt[6];
 };
 
-// Work counters of a propagate launch: warp-aggregated, then block-aggregated,
-// then one atomic per counter and block.
+// Work counters of a propagate launch: warp-aggregated (one REDUX per
+// counter), then block-aggregated, then one atomic per counter and block.
 KP_DEV void count_flush(KpCtl* ctl, uint32_t* c, uint32_t* cnt, int lane) {
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) c[k] += __shfl_down_sync(0xFFFFFFFFu, c[k], off);
-    }
+    for (int k = 0; k < 6; ++k) c[k] = __reduce_add_sync(0xFFFFFFFFu, c[k]);
     if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < 6; ++k)
@@ -193,7 +190,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
             const uint32_t i = c0 + p;
             uint32_t key = 0;
             if (p < CH && i < n_items) {
-                const uint32_t f = i / lam;
+                const uint32_t f = frontier_pos(P, i);
                 const uint32_t br = i - f * lam;
                 KP_ASSERT(f < ctl->n_va, 10);
                 const uint32_t node = va[f];
@@ -478,7 +475,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 acc_p[k] = 0.0f;
                 uint32_t vbad = 0u;
                 if (i < cend) {
-                    const uint32_t f = i / lam;
+                    const uint32_t f = frontier_pos(P, i);
                     const uint32_t br = i - f * lam;
                     KP_ASSERT(f < ctl->n_va, 10);
                     node[k] = va[f];
@@ -1190,7 +1187,7 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         const uint32_t abits = B.vu_acc[sl];
         B.dt[id] = B.vu_dt[sl];
         B.acc[id] = abits;
-        const uint32_t par = va[sl / lam];
+        const uint32_t par = va[frontier_pos(P, sl)];
         const uint32_t reg = B.vu_region[sl];
         B.region[id] = reg;
         B.parent[id] = static_cast<int32_t>(par);

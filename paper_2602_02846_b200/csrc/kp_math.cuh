@@ -301,6 +301,12 @@ __host__ __device__ constexpr bool closed_form() { return MODEL == 0 || MODEL ==
 KP_DEV long long len_fixed(float d) { return __float2ll_rn(d * 0x1p40f); }
 KP_DEV float fixed_len(long long s) { return __ll2float_rn(s) * 0x1p-40f; }
 
+// Frontier position of V_U slot i (slot = position * lambda + branch): a
+// shift when lambda is a power of two (every bundled scene), else a division.
+KP_DEV uint32_t frontier_pos(const KpProblem& P, uint32_t i) {
+    return P.lam_shift >= 0 ? (i >> P.lam_shift) : i / static_cast<uint32_t>(P.lambda);
+}
+
 // Number of RK4 steps of a segment: samples at 0, h, ..., dt.
 KP_DEV int step_count(const KpProblem& P, float dt) {
     const int S = static_cast<int>(ceilf(dt / P.h));

@@ -68,6 +68,7 @@ struct KpProblem {
     double t_prop_d;
     float inv_m, grav, cx, cy, cz, inv_ix, inv_iy, inv_iz;
     int32_t lambda, i_max, rng_kind, deact;
+    int32_t lam_shift;       // log2(lambda) when lambda is a power of two, else -1
     uint32_t capacity;       // t_e
     uint32_t max_slots;      // V_U slot buffer (multiple of 32)
     float x_init[KP_MAX_N];

@@ -14,6 +14,10 @@ for cfg in narrow_dubins6 building_quad12; do
   timeout 600 python bench.py --config $cfg --no-cpu-baseline > $OUT/bench_$cfg.json 2> $OUT/bench_$cfg.err
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+for cfg in building_quad12 narrow_dubins6 forest_di6; do
+  timeout 600 python bench.py --sweep --config $cfg --steps 5 --warmup 3 > $OUT/sweep_$cfg.json 2> $OUT/sweep_$cfg.err
+done
+timeout 600 python bench.py --batch 64 --lanes 8 > $OUT/bench_batch.json 2> $OUT/bench_batch.err
 python scripts/trace_gpu.py forest_di6 > $OUT/trace_forest_di6.txt 2>&1
 python scripts/trace_gpu.py building_quad12 1.0 > $OUT/trace_building_quad12.txt 2>&1
 python scripts/trace_gpu.py narrow_dubins6 > $OUT/trace_narrow_dubins6.txt 2>&1
@@ -28,6 +32,10 @@ for spec in "forest_di6 40" "building_quad12 30" "narrow_dubins6 40"; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_propagate -s $(( $2 - 3 )) -c 1 \
      -o $OUT/prop_$1 -f python scripts/prof_run.py $1 $2 > $OUT/ncu_prop_$1.log 2>&1
 done
+# the saturated Quad12 propagate (BASELINE config 5 at 2^22 items)
+timeout 300 python scripts/prof_sweep.py building_quad12 22 > $OUT/plain_sweep.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_propagate -s 2 -c 1 \
+   -o $OUT/prop_sweep_building_quad12 -f python scripts/prof_sweep.py building_quad12 22 > $OUT/ncu_sweep.log 2>&1
 timeout 300 python scripts/prof_run.py forest_di6 40 > /dev/null 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_select -s 74 -c 2 \
    -o $OUT/sel_forest_di6 -f python scripts/prof_run.py forest_di6 40 > $OUT/ncu_sel.log 2>&1

@@ -63,7 +63,8 @@ def fp32_share(rep):
 
 tr = {}
 for scene, fn in [("forest_di6", "ncu_prop_forest_di6"), ("building_quad12", "ncu_prop_building_quad12"),
-                  ("narrow_dubins6", "ncu_prop_narrow_dubins6"), ("forest_di6_select", "ncu_sel_forest_di6")]:
+                  ("narrow_dubins6", "ncu_prop_narrow_dubins6"), ("forest_di6_select", "ncu_sel_forest_di6"),
+                  ("building_quad12_sweep_2^22", "ncu_prop_sweep_building_quad12")]:
     path = f"profiles/{tag}/{fn}.txt"
     if not os.path.exists(path):
         continue

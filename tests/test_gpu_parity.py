@@ -242,12 +242,13 @@ def test_whole_run_bit_identical_propagate_paths(scene, iters, mode, monkeypatch
         assert rg[k] == ro[k], (k, rg[k], ro[k])
 
 
-@pytest.mark.parametrize("t_prop,h,lam", [(0.02, 0.02, 32), (2.0, 0.02, 4), (0.5, 0.02, 1)])
+@pytest.mark.parametrize("t_prop,h,lam", [(0.02, 0.02, 32), (2.0, 0.02, 4), (0.5, 0.02, 1), (0.5, 0.02, 5)])
 @pytest.mark.parametrize("mode", ["sample_parallel", "step_sorted"])
 def test_whole_run_bit_identical_rollout_lengths(t_prop, h, lam, mode, monkeypatch):
     """Rollout-length extremes on the double integrator's propagate paths: one
     sample per rollout (t_prop = h), up to 101 samples (past the step-count
-    sort's 64 buckets), lambda = 1."""
+    sort's 64 buckets), lambda = 1 and lambda = 5 (not a power of two: slot ->
+    frontier position by division)."""
     if mode == "step_sorted":
         monkeypatch.setenv("KP_FLAT", "0")
     else:
