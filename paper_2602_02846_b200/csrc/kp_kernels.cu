@@ -979,7 +979,7 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
 // (a lone query's latency win; the batch engine's concurrent lanes use the
 // plain variant, which also needs fewer registers)
 template <bool SPEC>
-__global__ void __launch_bounds__(KP_SELECT_THREADS, SPEC ? 5 : 8) k_select_reduce(KpProblem P, KpBuffers B) {
+__global__ void __launch_bounds__(KP_SELECT_THREADS, (SPEC ? 5 : 8) * 256 / KP_SELECT_THREADS) k_select_reduce(KpProblem P, KpBuffers B) {
     pdl_wait();
     pdl_trigger();
     select_reduce_phase<SPEC>(P, B);
