@@ -278,3 +278,78 @@ def test_quadcopter_split_long_rollouts(monkeypatch):
     ro = o.run(budget_s=0.0, max_iterations=iters, stop_first=0)
     for k in ("best_cost", "node_count", "propagations_valid", "nodes_committed", "timeline_len"):
         assert rg[k] == ro[k], (k, rg[k], ro[k])
+
+
+def _item_parity(s, ps, seed, it=5):
+    """debug_propagate on the device vs the Mirror32 restatement, bit-exact."""
+    k = ps.shape[0]
+    rng = np.random.default_rng(seed)
+    pacc = (rng.random(k) * 5).astype(np.float32)
+    ids = rng.integers(0, 1 << 20, k).astype(np.uint32)
+    brs = rng.integers(0, 32, k).astype(np.uint32)
+    with Planner(s, seed=seed) as g:
+        d = g.debug_propagate(ps, pacc, ids, brs, iteration=it)
+    o = kpo.Oracle(s, kpo.MIRROR32, seed=seed).propagate_items(ps.astype(np.float64), pacc.astype(np.float64),
+                                                                ids, brs, it)
+    gv, ov = d["valid"] == 1, o["valid"] == 1
+    np.testing.assert_array_equal(d["valid"], o["valid"])
+    np.testing.assert_array_equal(d["state"][gv].astype(np.float64), o["state"][ov])
+    np.testing.assert_array_equal(d["acc"][gv].astype(np.float64), o["acc"][ov])
+    np.testing.assert_array_equal(d["region"][gv], o["region"][ov])
+    np.testing.assert_array_equal(d["steps"][gv], o["steps"][ov])
+    return gv
+
+
+def test_velocity_bounds_checked_once_per_item():
+    """Double integrator: the device checks the velocity bounds once per item,
+    at the last sample (kp_math.cuh vel_ok_at_end; v(t) = fma(u, t, v0) is
+    monotone), the restatement at every sample.  Parents on, just inside and
+    a few ulps inside the velocity bounds, controls pushing both ways: the
+    verdicts (and every valid item's bits) must be the same."""
+    s = scenarios.load("forest_di6", max_slots=1 << 16, capacity=1 << 14)
+    rng = np.random.default_rng(3)
+    base = _random_parents(s, 512, rng)
+    hi = np.array([b[1] for b in s["problem"]["state_bounds"]], np.float32)
+    lo = np.array([b[0] for b in s["problem"]["state_bounds"]], np.float32)
+    rows = []
+    for r, x in enumerate(base):
+        x = x.copy()
+        d = 3 + r % 3
+        edge = [hi[d], lo[d], np.nextafter(hi[d], np.float32(0)), np.nextafter(lo[d], np.float32(0)),
+                hi[d] - np.float32(1e-3), lo[d] + np.float32(1e-3)][r % 6]
+        x[d] = edge
+        rows.append(x)
+    ps = np.stack(rows).astype(np.float32)
+    gv = _item_parity(s, ps, seed=17)
+    assert 0 < gv.sum() < len(gv)  # both verdicts occur
+
+
+def test_small_angle_sincos_fast_path_boundary():
+    """Quadcopter roll / pitch sincos: the device skips the range reduction when
+    |x * 2/pi| < 1/2 (bit-identical by construction).  Roll / pitch bounds
+    widened to +-1.2 rad and parents placed around pi/4 (the fast-path edge),
+    so stage angles fall on both sides of it: bit-exact against the
+    restatement's general recipe."""
+    s = scenarios.load("building_quad12", max_slots=1 << 16, capacity=1 << 14)
+    for d in (6, 7):
+        s["problem"]["state_bounds"][d] = [-1.2, 1.2]
+    rng = np.random.default_rng(5)
+    ps = _random_parents(s, 1024, rng)
+    edge = np.float32(np.pi / 4)
+    for r in range(len(ps)):
+        ps[r, 6 + r % 2] = np.float32(edge + (r % 7 - 3) * 1e-4) * (1 if r % 3 else -1)
+    _item_parity(s, ps, seed=23)
+
+
+def test_angle_wrap_all_angles_at_once():
+    """One wrap test for all of a model's angles (max |a| >= pi): headings on
+    and around +-pi, so single steps cross the wrap; bit-exact against the
+    restatement's per-angle wrap_angle."""
+    for scene, d in (("narrow_dubins6", 3), ("building_quad12", 8)):
+        s = scenarios.load(scene, max_slots=1 << 16, capacity=1 << 14)
+        rng = np.random.default_rng(9)
+        ps = _random_parents(s, 1024, rng)
+        pi = np.float32(np.pi)
+        for r in range(len(ps)):
+            ps[r, d] = [pi, -np.nextafter(pi, np.float32(0)), np.float32(3.1), np.float32(-3.1)][r % 4]
+        _item_parity(s, ps, seed=29)
