@@ -57,7 +57,15 @@ cudaError_t launch_reintegrate(const KpProblem& P, const KpBuffers& B, const int
 
 namespace {
 
-constexpr int KP_GRAPH_ITERS = 8;
+// Iterations per captured graph.  Consecutive graphs on the stream cannot
+// chain their kernels with programmatic dependent launch, so every graph
+// boundary costs ~6 us more than an iteration boundary inside a graph; after
+// the device raises done, the rest of the graph runs as no-op kernels.  32
+// measured best of 8 / 16 / 32 (forest queries +2 %, time to first solution
+// 0.622 -> 0.610 ms, profiles/README.md).
+#ifndef KP_GRAPH_ITERS
+#define KP_GRAPH_ITERS 32
+#endif
 
 struct KpError : std::runtime_error {
     int code;
