@@ -1,4 +1,7 @@
-# A/B of environment variants on given scenes: bash scripts/r2_env_ab.sh TAG "SCENES" "ENV..." ...
+#!/bin/bash
+# A/B of environment-variable variants (KP_FLAT_MAX, KP_PROP_GRID, KP_SEL_GRID, ...)
+# on the same library, two rounds each, with ab_perf.py:
+#   bash scripts/ab_env.sh TAG "SCENES" "ENV=a" "ENV=b ENV2=c" ...   (under gpurun)
 set -u
 TAG=$1; SCENES=$2; shift 2; OUT=gpurun_out/$TAG; mkdir -p $OUT
 for r in 1 2; do

@@ -1,22 +1,31 @@
-"""Opcode mix of an ncu source page (sass rows) weighted by executed warp instructions."""
+"""Opcode mix of an .ncu-rep (SASS source page), weighted by executed warp / thread instructions.
+python scripts/ncu_opmix.py REP [N]"""
 import collections
 import csv
+import io
+import subprocess
 import sys
 
-agg = collections.Counter()
-thr = collections.Counter()
-for r in csv.reader(open(sys.argv[1])):
-    if len(r) < 10 or r[0] not in ("",) or r[2] in ("...", "") or not r[2].startswith("0x"):
+rep = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(txt)))
+hdr = next(r for r in rows if "Instructions Executed" in r)
+ie, te = hdr.index("Instructions Executed"), hdr.index("Thread Instructions Executed")
+agg, thr = collections.Counter(), collections.Counter()
+for r in rows:
+    if len(r) <= te or not r[0].startswith("0x"):
         continue
-    if r[7] in ("-", ""):
-        continue
-    ins = r[3].strip()
+    ins = r[1].strip()
     if ins.startswith("@"):
         ins = ins.split(None, 1)[1]
-    op = ins.split()[0]
-    agg[op] += int(r[7])
-    thr[op] += int(r[8])
-tot = sum(agg.values())
-print("total", tot)
-for op, n in agg.most_common(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
-    print(f"{op:24s} {100*n/tot:5.1f}%  simt {thr[op]/n:5.1f}")
+    try:
+        agg[ins.split()[0]] += int(r[ie])
+        thr[ins.split()[0]] += int(r[te])
+    except ValueError:
+        pass
+tot, tt = sum(agg.values()), sum(thr.values())
+print(f"warp instructions {tot}, thread instructions {tt}, SIMT {tt / max(1, tot):.2f}")
+for op, v in agg.most_common(n):
+    print(f"{op:22s} {100 * v / tot:6.2f}% warp {100 * thr[op] / tt:6.2f}% thread")
