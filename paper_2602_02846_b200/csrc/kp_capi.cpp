@@ -60,11 +60,20 @@ namespace {
 // Iterations per captured graph.  Consecutive graphs on the stream cannot
 // chain their kernels with programmatic dependent launch, so every graph
 // boundary costs ~6 us more than an iteration boundary inside a graph; after
-// the device raises done, the rest of the graph runs as no-op kernels.  32
-// measured best of 8 / 16 / 32 (forest queries +2 %, time to first solution
-// 0.622 -> 0.610 ms, profiles/README.md).
+// the device raises done, the rest of the graph runs as no-op kernels, which
+// the next query on the stream waits behind.  A solve therefore launches
+// graphs of KP_GRAPH_HEAD iterations first (a first solution typically comes
+// within them: few trailing no-ops for stop-at-first-solution queries), then
+// graphs of KP_GRAPH_ITERS (forest 100 ms queries +2 %, time to first
+// solution 0.622 -> 0.610 ms over graphs of 8 only, profiles/README.md).
 #ifndef KP_GRAPH_ITERS
 #define KP_GRAPH_ITERS 32
+#endif
+#ifndef KP_GRAPH_HEAD
+#define KP_GRAPH_HEAD 8
+#endif
+#ifndef KP_HEAD_LAUNCHES
+#define KP_HEAD_LAUNCHES 4
 #endif
 
 struct KpError : std::runtime_error {
@@ -89,7 +98,8 @@ struct kp_planner {
     int grid_prop = 0, grid_sel = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t fetch_stream = nullptr;  // result fetch that need not wait for trailing no-op launches
-    cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graph = nullptr;       // KP_GRAPH_ITERS iterations
+    cudaGraphExec_t graph_head = nullptr;  // KP_GRAPH_HEAD iterations: a solve's first launches
     uint32_t* host_done = nullptr;  // pinned, mapped
     std::vector<void*> allocs;
     std::string err;
@@ -117,6 +127,7 @@ struct kp_planner {
     ~kp_planner() {
         if (stream) cudaStreamSynchronize(stream);
         if (graph) cudaGraphExecDestroy(graph);
+        if (graph_head) cudaGraphExecDestroy(graph_head);
         for (auto* e : ev)
             if (e) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
@@ -463,12 +474,25 @@ std::vector<uint8_t> build_env(KpProblem& P, const std::vector<float>& boxes, co
 }
 
 void capture_graph(kp_planner* pl) {
-    cudaGraph_t g = nullptr;
-    cuda_check(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
-    for (int i = 0; i < KP_GRAPH_ITERS; ++i) kp::launch_iteration(pl->P, pl->B, pl->grid_prop, pl->grid_sel, pl->stream, 7);
-    cuda_check(cudaStreamEndCapture(pl->stream, &g), "cudaStreamEndCapture");
-    cuda_check(cudaGraphInstantiate(&pl->graph, g, 0), "cudaGraphInstantiate");
-    cudaGraphDestroy(g);
+    for (int which = 0; which < 2; ++which) {
+        const int iters = which ? KP_GRAPH_HEAD : KP_GRAPH_ITERS;
+        cudaGraph_t g = nullptr;
+        cuda_check(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        for (int i = 0; i < iters; ++i) kp::launch_iteration(pl->P, pl->B, pl->grid_prop, pl->grid_sel, pl->stream, 7);
+        cuda_check(cudaStreamEndCapture(pl->stream, &g), "cudaStreamEndCapture");
+        cuda_check(cudaGraphInstantiate(which ? &pl->graph_head : &pl->graph, g, 0), "cudaGraphInstantiate");
+        cudaGraphDestroy(g);
+    }
+}
+
+// Launch the solve's n-th graph (head graphs first); returns its iterations.
+int launch_graph(kp_planner* pl, int n) {
+    const bool head = n < KP_HEAD_LAUNCHES;
+    cuda_check(cudaGraphLaunch(head ? pl->graph_head : pl->graph, pl->stream), "cudaGraphLaunch");
+    pl->graph_launches += 1;
+    const int iters = head ? KP_GRAPH_HEAD : KP_GRAPH_ITERS;
+    pl->kernel_launches += 3 * iters;
+    return iters;
 }
 
 void reset_async(kp_planner* pl, uint64_t seed) {
@@ -854,9 +878,7 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
                     }
                     if (*done) break;
                 }
-                cuda_check(cudaGraphLaunch(pl->graph, pl->stream), "cudaGraphLaunch");
-                pl->graph_launches += 1;
-                pl->kernel_launches += 3 * KP_GRAPH_ITERS;
+                launch_graph(pl, n_launched);
                 cuda_check(cudaEventRecord(inflight[n_launched & 1], pl->stream), "event");
                 ++n_launched;
             }
@@ -995,7 +1017,9 @@ int kp_batch_create(const kp_problem_desc* problem, const kp_config_desc* config
                 kp::set_flat_limit(pl->P, pl->grid_prop);
                 pl->P.sel_spec = 0;  // throughput-bound: the speculative loads cost more than they hide
                 if (pl->graph) cudaGraphExecDestroy(pl->graph);
+                if (pl->graph_head) cudaGraphExecDestroy(pl->graph_head);
                 pl->graph = nullptr;
+                pl->graph_head = nullptr;
                 capture_graph(pl);
             }
         } catch (const KpError& e) {
@@ -1059,10 +1083,8 @@ int kp_batch_solve(kp_batch* b, const uint64_t* seeds, size_t k, double budget_s
                         cudaEvent_t e = pl->ev[2 + (L.launched & 1)];
                         const bool slot_free = L.launched < 2 || cudaEventQuery(e) == cudaSuccess;
                         if (slot_free) {
-                            cuda_check(cudaGraphLaunch(pl->graph, pl->stream), "cudaGraphLaunch");
+                            launch_graph(pl, L.launched);
                             cuda_check(cudaEventRecord(e, pl->stream), "event");
-                            pl->graph_launches += 1;
-                            pl->kernel_launches += 3 * KP_GRAPH_ITERS;
                             ++L.launched;
                         }
                     }
