@@ -275,8 +275,8 @@ typedef struct kp_trace_entry {
     uint64_t t_ns;
     uint32_t iteration, items, live, frontier, nodes, committed;
     /* in-graph kernel stamps, ns since solve start: block-0 entry of
-     * propagate / select_reduce / select_scatter, last-block exit of
-     * select_reduce (t_ns is the scatter's last block = the boundary) */
+     * propagate / select_reduce, entry of the select_scatter block that
+     * closes the iteration (t_sel_end == t_scat; t_ns = the boundary) */
     uint32_t t_prop, t_sel, t_sel_end, t_scat;
 } kp_trace_entry;
 

@@ -718,6 +718,7 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         pl->grid_prop = pl->sms * occ;
         if (const char* g = std::getenv("KP_PROP_GRID")) pl->grid_prop = std::max(1, std::min(pl->grid_prop, std::atoi(g)));
         pl->grid_sel = pl->sms * (1024 / KP_SELECT_THREADS);
+        if (const char* g = std::getenv("KP_SEL_GRID")) pl->grid_sel = std::max(1, std::atoi(g));  // A/B hook
         kp::set_flat_limit(pl->P, pl->grid_prop);
         B.prop_scratch = pl->dalloc<float>(static_cast<size_t>(pl->grid_prop) * (P.n + 1) * 1024);
 

@@ -987,24 +987,57 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS, (SPEC ? 5 : 8) * 256 / KP_S
 
 // Close an iteration: counts, stats, best / timeline / TTFS
 // from %globaltimer, trace record, termination.  One thread of the last block.
+// The control-block fields the boundary reads, all written before the
+// scatter kernel starts (by the previous boundary, k_start, propagate and
+// select_reduce) except `best`, which goal commits lower during the scatter.
+// Every scatter block's thread 0 loads them beside its own control-block
+// reads (the same round trip) and parks them in shared memory, so the closing
+// block needs no further round trip unless a goal node was committed.
+struct BoundaryIn {
+    unsigned long long best, tl_best, t_start, first_ns, deadline, t_prop, t_sel;
+    unsigned long long st_att, st_com, st_drop;
+    uint32_t tl_len, max_iter_abs, stop_first, n_valid;
+};
+
+KP_DEV BoundaryIn load_boundary_in(const KpCtl* ctl) {
+    BoundaryIn b;
+    b.best = ctl->best;
+    b.tl_best = ctl->tl_best;  // == timeline_len ? timeline[timeline_len - 1].best : ~0
+    b.t_start = ctl->t_start_ns;
+    b.first_ns = ctl->first_ns;
+    b.deadline = ctl->deadline_ns;
+    b.t_prop = ctl->t_prop_ns;
+    b.t_sel = ctl->t_sel_ns;
+    b.st_att = ctl->stats.attempted;
+    b.st_com = ctl->stats.committed;
+    b.st_drop = ctl->stats.dropped_capacity;
+    b.tl_len = ctl->timeline_len;
+    b.max_iter_abs = ctl->max_iter_abs;
+    b.stop_first = ctl->stop_first;
+    b.n_valid = ctl->n_valid_iter;
+    return b;
+}
+
+// bin: the prefetched inputs; best: the current best (re-read by the caller
+// when a goal node was committed this iteration); t_scat: the closing
+// block's entry stamp.
 KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t it, uint32_t n_items,
                                uint32_t tot_keep, uint32_t tot_va, uint32_t tot_commit, uint32_t n_nodes,
-                               uint32_t accepted) {
+                               uint32_t accepted, const BoundaryIn& bin, unsigned long long best,
+                               unsigned long long t_scat) {
     KpCtl* ctl = B.ctl;
     const uint32_t S = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
-    // all control-block reads first (one batch of independent loads), then writes
     const unsigned long long now = globaltimer();
     const uint32_t it1 = it + 1;
-    const unsigned long long best = ctl->best;
-    const uint32_t tl_len = ctl->timeline_len;
-    const unsigned long long prev = ctl->tl_best;  // == tl_len ? timeline[tl_len - 1].best : ~0
-    const unsigned long long t_start = ctl->t_start_ns, first_ns = ctl->first_ns, deadline = ctl->deadline_ns;
-    const unsigned long long t_prop = ctl->t_prop_ns, t_sel = ctl->t_sel_ns, t_scat = ctl->t_scat_ns;
-    const uint32_t max_iter_abs = ctl->max_iter_abs, stop_first = ctl->stop_first;
-    const unsigned long long st_att = ctl->stats.attempted, st_com = ctl->stats.committed;
-    const unsigned long long st_drop = ctl->stats.dropped_capacity;
-    const uint32_t n_valid = ctl->n_valid_iter;
+    const uint32_t tl_len = bin.tl_len;
+    const unsigned long long prev = bin.tl_best;
+    const unsigned long long t_start = bin.t_start, first_ns = bin.first_ns, deadline = bin.deadline;
+    const unsigned long long t_prop = bin.t_prop, t_sel = bin.t_sel;
+    const uint32_t max_iter_abs = bin.max_iter_abs, stop_first = bin.stop_first;
+    const unsigned long long st_att = bin.st_att, st_com = bin.st_com;
+    const unsigned long long st_drop = bin.st_drop;
+    const uint32_t n_valid = bin.n_valid;
     const uint32_t n_live1 = tot_keep + accepted, n_va1 = tot_va + accepted, n_nodes1 = n_nodes + accepted;
     KP_ASSERT(n_nodes1 <= P.capacity && n_live1 <= n_nodes1 && n_va1 <= n_live1, 40);
     const unsigned long long items = static_cast<unsigned long long>(n_va1) * lam;
@@ -1080,9 +1113,16 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     // every control-block read up front: one round trip
     const uint32_t done = ctl->done, it = ctl->iter, n_live = ctl->n_live, n_items = ctl->n_items;
     const uint32_t n_adm = ctl->n_adm_iter, n_nodes = ctl->n_nodes;
+    __shared__ unsigned int s_last, s_goal;
+    __shared__ BoundaryIn s_bin;
+    __shared__ unsigned long long s_t0;
+    if (threadIdx.x == 0) {  // the boundary's inputs, in the same round trip as the fields above
+        s_bin = load_boundary_in(ctl);
+        s_goal = 0;
+        s_t0 = globaltimer();
+    }
     if (done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_scat_ns = globaltimer();
-    __shared__ unsigned int s_last;
     __shared__ uint32_t s_red[6][KP_SELECT_THREADS / 32];
     const SelLayout ly = sel_layout(n_live, n_items, n_adm);  // as select_reduce
     const uint32_t n_tiles = ly.n_tiles;
@@ -1197,8 +1237,10 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         live_n[tot_keep + rank] = make_uint4(id, reg, abits, par);
         live_si_n[tot_keep + rank] = KP_ST_ACTIVE;
         va_n[tot_va + rank] = id;
-        if (goal)  // Alg. 4 lines 5-7
+        if (goal) {  // Alg. 4 lines 5-7
             atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
+            s_goal = 1u;
+        }
     };
     for (uint32_t tile = tb; tile < te; ++tile) {
         const Elem el = tile == tb ? first : load_elem(tile);
@@ -1244,18 +1286,24 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     // last block closes the iteration: the barrier orders the block's writes
     // before thread 0's gpu-scope release (cumulative), the acquire of the
     // last arriver makes every block's writes visible to it
+    // The ticket also carries, from bit 20 up, the number of blocks that
+    // committed a goal node: without one, `best` is still the prefetched value.
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned int prev;
-        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctl->ticket_b) : "memory");
-        s_last = prev == n_part - 1;
+        const unsigned int add = 1u + (s_goal ? (1u << 20) : 0u);
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(prev) : "l"(&ctl->ticket_b), "r"(add) : "memory");
+        s_last = (prev & 0xFFFFFu) == n_part - 1;
+        if (s_last) {
+            const bool any_goal = s_goal || (prev >> 20) != 0u;
+            const unsigned long long best = any_goal ? *reinterpret_cast<volatile unsigned long long*>(&ctl->best)
+                                                     : s_bin.best;
+            iteration_boundary(P, B, it, n_items, tot_keep, tot_va, tot_commit, n_nodes, accepted, s_bin, best, s_t0);
+        }
     }
-    __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
-    iteration_boundary(P, B, it, n_items, tot_keep, tot_va, tot_commit, n_nodes, accepted);
 }
 
-__global__ void __launch_bounds__(KP_SELECT_THREADS) k_select_scatter(KpProblem P, KpBuffers B) {
+__global__ void __launch_bounds__(KP_SELECT_THREADS, 1024 / KP_SELECT_THREADS) k_select_scatter(KpProblem P, KpBuffers B) {
     pdl_wait();
     pdl_trigger();
     scatter_phase(P, B);

@@ -115,8 +115,8 @@ struct KpTraceRec {
     unsigned long long t_ns;
     uint32_t iteration, items, live, frontier, nodes, committed;
     // in-graph kernel timestamps (ns since solve start): block 0 entry of
-    // propagate / select_reduce / select_scatter and the last-block exit of
-    // select_reduce; the boundary itself is t_ns (scatter last block)
+    // propagate and select_reduce, entry of the select_scatter block that
+    // closes the iteration (t_sel_end == t_scat); the boundary itself is t_ns
     uint32_t t_prop, t_sel, t_sel_end, t_scat;
 };
 
