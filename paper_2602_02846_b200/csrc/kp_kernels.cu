@@ -66,6 +66,49 @@ KP_DEV Env stage_env(const KpProblem& P, const KpBuffers& B) {
     return env_view(P);
 }
 
+// The propagate kernels stage the blob with the bulk-copy (TMA) engine
+// instead: thread 0 arms an mbarrier with the blob's byte count and issues
+// cp.async.bulk global -> shared; the block waits on the barrier (env_wait)
+// only before its first obstacle test, so the copy overlaps the PDL wait,
+// the control-block round trip and the sampling, and no thread spends issue
+// slots on the copy.
+__shared__ __align__(8) unsigned long long kp_env_bar;
+
+KP_DEV uint32_t env_bar_addr() { return static_cast<uint32_t>(__cvta_generic_to_shared(&kp_env_bar)); }
+
+KP_DEV Env stage_env_async(const KpProblem& P, const KpBuffers& B) {
+    if (threadIdx.x == 0) {
+        const uint32_t bar = env_bar_addr();
+        const uint32_t dst = env_saddr();
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(P.env_bytes) : "memory");
+        constexpr uint32_t CHUNK = 32768;  // bytes per bulk copy (multiples of 16)
+        for (uint32_t off = 0; off < P.env_bytes; off += CHUNK) {
+            const uint32_t n = min(CHUNK, P.env_bytes - off);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
+                "l"(reinterpret_cast<const unsigned char*>(B.env) + off), "r"(n), "r"(bar)
+                : "memory");
+        }
+    }
+    __syncthreads();  // the barrier is initialised before any thread waits on it
+    return env_view(P);
+}
+
+// Wait for the environment's bulk copy (phase 0 of the barrier: returns at
+// once after the first completion, so repeated calls are free).
+KP_DEV void env_wait() {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "ENV_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        "@!p bra ENV_WAIT_%=;\n"
+        "}\n" ::"r"(env_bar_addr())
+        : "memory");
+}
+
 // Propagate (Alg. 2).  Work is claimed by blocks in chunks of 256*G slots
 // (dynamic cursor).  Per chunk: (1) every thread draws (u, dt) for G slots
 // (convergent RNG) into shared memory; (2) block counting sort of the chunk
@@ -232,6 +275,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
             sh.perm[pos] = static_cast<uint16_t>(p);
         }
         __syncthreads();
+        env_wait();
         // (3) integrate groups of 32 consecutive sorted slots per warp.  When a
         // warp has several groups (the launch spans more than one wave) and at
         // least a quarter of the previous iteration's rollouts were invalid, the
@@ -539,6 +583,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 if (threadIdx.x == T - 1) off[FB] = o;
             }
             __syncthreads();
+            env_wait();
             {
                 // (3) chunks of K consecutive samples (one item each), interleaved
                 // over the block: round r, thread t takes chunk r*T + t, so every
@@ -661,7 +706,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
 
 template <int MODEL>
 __global__ void __launch_bounds__(PropCfg<MODEL>::T, PropCfg<MODEL>::MIN_BLOCKS) k_propagate(KpProblem P, KpBuffers B) {
-    const Env E = stage_env(P, B);  // constant data: overlaps the predecessor's tail
+    const Env E = stage_env_async(P, B);  // constant data: overlaps the predecessor's tail
     pdl_wait();
     pdl_trigger();
     unsigned char* const dyn = reinterpret_cast<unsigned char*>(kp_env_smem);
@@ -670,10 +715,12 @@ __global__ void __launch_bounds__(PropCfg<MODEL>::T, PropCfg<MODEL>::MIN_BLOCKS)
         // ones are issue-bound, where the step-sorted path runs fewer instructions
         if (P.flat_on && B.ctl->n_items <= P.flat_max) {
             flat_phase<MODEL>(P, B, E, dyn);
+            env_wait();  // no block exits with its bulk copy in flight
             return;
         }
     }
     propagate_phase<MODEL>(P, B, *reinterpret_cast<PropSmem<MODEL>*>(dyn + P.seq_base), E);
+    env_wait();
 }
 
 // Block-wide inclusive sum of three counters (blockDim == KP_SELECT_THREADS).
