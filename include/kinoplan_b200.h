@@ -286,6 +286,11 @@ int kp_get_trace(kp_planner* planner, kp_trace_entry* buf, size_t cap, size_t* l
  * so a caller can bracket work with its own CUDA events. */
 int kp_get_stream(kp_planner* planner, void** stream);
 
+/* Diagnostics of a library built with -DKP_STAMPS (scripts/stamps.py): the
+ * %globaltimer phase stamps of the last 64 iterations, 64 x 16 uint64 (row =
+ * iteration mod 64; columns in kp_kernels.cu).  KP_ERR_CONFIG otherwise. */
+int kp_debug_stamps(kp_planner* planner, uint64_t* out_64x16);
+
 /* ---- propagation sweep (BASELINE config 5) -------------------------------- */
 
 /* Replace the tree by a synthetic frontier of n_nodes valid states: positions

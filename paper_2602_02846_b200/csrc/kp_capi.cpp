@@ -32,6 +32,7 @@
 
 namespace kp {
 cudaError_t read_check_code(unsigned int* code);
+cudaError_t read_stamps(unsigned long long* out);
 cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_prop, int grid_sel, cudaStream_t st,
                              int which);
 cudaError_t set_propagate_smem(const KpProblem& P);
@@ -823,6 +824,17 @@ int kp_get_stream(kp_planner* pl, void** stream) {
     if (!pl || !stream) return KP_ERR_ARGUMENT;
     *stream = static_cast<void*>(pl->stream);
     return KP_OK;
+}
+
+int kp_debug_stamps(kp_planner* pl, uint64_t* out) {
+    if (!pl || !out) return KP_ERR_ARGUMENT;
+    return guard(pl, [&] {
+        cuda_check(cudaSetDevice(pl->device), "cudaSetDevice");
+        cuda_check(cudaStreamSynchronize(pl->stream), "sync");
+        const cudaError_t e = kp::read_stamps(reinterpret_cast<unsigned long long*>(out));
+        if (e == cudaErrorNotSupported) throw KpError(KP_ERR_CONFIG, "library built without -DKP_STAMPS");
+        cuda_check(e, "read stamps");
+    });
 }
 
 int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result* out) {

@@ -59,6 +59,37 @@ KP_DEV unsigned long long globaltimer() {
 KP_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 KP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Diagnostic build only (-DKP_STAMPS, scripts/stamps.py): %globaltimer stamps
+// of kernel phases per iteration (a ring of 64 iterations x 16 points) — block
+// 0's entry / PDL release / control-block arrival and the latest block exit
+// of each kernel, the closing scatter block's ticket and boundary.
+#ifdef KP_STAMPS
+__device__ unsigned long long kp_stamps[64][16];
+#define KP_STAMP_B0(it, k, t)                                                        \
+    do {                                                                            \
+        if (blockIdx.x == 0 && threadIdx.x == 0) kp_stamps[(it) & 63][k] = (t);     \
+    } while (0)
+#define KP_STAMP_MAX(it, k)                                                          \
+    do {                                                                            \
+        if (threadIdx.x == 0) atomicMax(&kp_stamps[(it) & 63][k], globaltimer());   \
+    } while (0)
+#define KP_T0 const unsigned long long kp_t_entry = globaltimer()
+#define KP_T1 const unsigned long long kp_t_pdl = globaltimer()
+#else
+#define KP_STAMP_B0(it, k, t) \
+    do {                      \
+    } while (0)
+#define KP_STAMP_MAX(it, k) \
+    do {                    \
+    } while (0)
+#define KP_T0 \
+    do {      \
+    } while (0)
+#define KP_T1 \
+    do {      \
+    } while (0)
+#endif
+
 // Stage the environment blob into shared memory (16-byte vector copies).
 KP_DEV Env stage_env(const KpProblem& P, const KpBuffers& B) {
     for (uint32_t i = threadIdx.x; i < P.env_bytes / 16; i += blockDim.x) kp_env_smem[i] = B.env[i];
@@ -706,9 +737,17 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
 
 template <int MODEL>
 __global__ void __launch_bounds__(PropCfg<MODEL>::T, PropCfg<MODEL>::MIN_BLOCKS) k_propagate(KpProblem P, KpBuffers B) {
+    KP_T0;
     const Env E = stage_env_async(P, B);  // constant data: overlaps the predecessor's tail
     pdl_wait();
+    KP_T1;
     pdl_trigger();
+#ifdef KP_STAMPS
+    const uint32_t it_s = B.ctl->iter;
+    KP_STAMP_B0(it_s, 0, kp_t_entry);
+    KP_STAMP_B0(it_s, 1, kp_t_pdl);
+    KP_STAMP_B0(it_s, 14, globaltimer());
+#endif
     unsigned char* const dyn = reinterpret_cast<unsigned char*>(kp_env_smem);
     if constexpr (closed_form<MODEL>()) {
         // small launches are latency-bound: flatten them into samples; large
@@ -716,11 +755,13 @@ __global__ void __launch_bounds__(PropCfg<MODEL>::T, PropCfg<MODEL>::MIN_BLOCKS)
         if (P.flat_on && B.ctl->n_items <= P.flat_max) {
             flat_phase<MODEL>(P, B, E, dyn);
             env_wait();  // no block exits with its bulk copy in flight
+            KP_STAMP_MAX(it_s, 2);
             return;
         }
     }
     propagate_phase<MODEL>(P, B, *reinterpret_cast<PropSmem<MODEL>*>(dyn + P.seq_base), E);
     env_wait();
+    KP_STAMP_MAX(it_s, 2);
 }
 
 // Block-wide inclusive sum of three counters (blockDim == KP_SELECT_THREADS).
@@ -1027,9 +1068,16 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
 // plain variant, which also needs fewer registers)
 template <bool SPEC>
 __global__ void __launch_bounds__(KP_SELECT_THREADS, (SPEC ? 5 : 8) * 256 / KP_SELECT_THREADS) k_select_reduce(KpProblem P, KpBuffers B) {
+    KP_T0;
     pdl_wait();
+    KP_T1;
     pdl_trigger();
+#ifdef KP_STAMPS
+    const uint32_t it_s = B.ctl->iter;
+    KP_STAMP_B0(it_s, 5, globaltimer());
+#endif
     select_reduce_phase<SPEC>(P, B);
+    KP_STAMP_MAX(it_s, 6);
 }
 
 // Close an iteration: counts, stats, best / timeline / TTFS
@@ -1250,6 +1298,7 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         }
     }
     const uint32_t tot_keep = acc[3], tot_va = acc[4], tot_commit = acc[5];
+    KP_STAMP_MAX(it, 15);  // diagnostic build: prefix pass done (latest block)
     const uint32_t remaining = P.capacity - n_nodes;
     const uint32_t accepted = tot_commit < remaining ? tot_commit : remaining;
     Cnt3 run{acc[0], acc[1], acc[2]};
@@ -1265,17 +1314,28 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         const uint32_t id = n_nodes + rank;
         KP_ASSERT(id < cap && sl < S && sl / lam < ctl->n_va, 30);
         KP_ASSERT(tot_keep + rank < cap && tot_va + rank < cap, 31);
-#pragma unroll 4
-        for (int d = 0; d < P.n; ++d)
-            B.state[static_cast<size_t>(d) * cap + id] = B.vu_state[static_cast<size_t>(d) * S + sl];
-#pragma unroll 4
-        for (int d = 0; d < P.m; ++d)
-            B.ctrl[static_cast<size_t>(d) * cap + id] = B.vu_ctrl[static_cast<size_t>(d) * S + sl];
+        // every load of the slot record first, then the stores: interleaved,
+        // the possible aliasing of the float arrays kept each load behind the
+        // previous store — a dozen dependent L2 round trips per committed node
+        float xs[KP_MAX_N], us[KP_MAX_M];
+#pragma unroll
+        for (int d = 0; d < KP_MAX_N; ++d)
+            if (d < P.n) xs[d] = B.vu_state[static_cast<size_t>(d) * S + sl];
+#pragma unroll
+        for (int d = 0; d < KP_MAX_M; ++d)
+            if (d < P.m) us[d] = B.vu_ctrl[static_cast<size_t>(d) * S + sl];
         const uint32_t abits = B.vu_acc[sl];
-        B.dt[id] = B.vu_dt[sl];
-        B.acc[id] = abits;
+        const float dts = B.vu_dt[sl];
         const uint32_t par = va[frontier_pos(P, sl)];
         const uint32_t reg = B.vu_region[sl];
+#pragma unroll
+        for (int d = 0; d < KP_MAX_N; ++d)
+            if (d < P.n) B.state[static_cast<size_t>(d) * cap + id] = xs[d];
+#pragma unroll
+        for (int d = 0; d < KP_MAX_M; ++d)
+            if (d < P.m) B.ctrl[static_cast<size_t>(d) * cap + id] = us[d];
+        B.dt[id] = dts;
+        B.acc[id] = abits;
         B.region[id] = reg;
         B.parent[id] = static_cast<int32_t>(par);
         B.link[id] = make_uint4(par, reg, abits, 0u);
@@ -1296,6 +1356,7 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         const bool in_slots = el.in_slots;
         Cnt3 tot;
         const Cnt3 inc = block_scan3(x, &tot);  // (barrier: every lane has read its goal bit)
+        if (tile == tb) KP_STAMP_MAX(it, 3);  // diagnostic build: first scan done (latest block)
         const uint32_t pk = run.k + inc.k - x.k;
         const uint32_t pv = run.v + inc.v - x.v;
         const uint32_t pc = run.c + inc.c - x.c;  // commits before this element (slot order)
@@ -1333,26 +1394,51 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     // last block closes the iteration: the barrier orders the block's writes
     // before thread 0's gpu-scope release (cumulative), the acquire of the
     // last arriver makes every block's writes visible to it
+    KP_STAMP_MAX(it, 4);  // diagnostic build: writes issued (latest block)
     // The ticket also carries, from bit 20 up, the number of blocks that
     // committed a goal node: without one, `best` is still the prefetched value.
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned int prev;
         const unsigned int add = 1u + (s_goal ? (1u << 20) : 0u);
+#ifdef KP_STAMPS
+        const unsigned long long t_pre = globaltimer();
+        atomicMax(&kp_stamps[it & 63][13], t_pre);
+#endif
         asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(prev) : "l"(&ctl->ticket_b), "r"(add) : "memory");
         s_last = (prev & 0xFFFFFu) == n_part - 1;
         if (s_last) {
+#ifdef KP_STAMPS
+            kp_stamps[it & 63][10] = t_pre;
+            kp_stamps[it & 63][11] = globaltimer();
+#endif
             const bool any_goal = s_goal || (prev >> 20) != 0u;
             const unsigned long long best = any_goal ? *reinterpret_cast<volatile unsigned long long*>(&ctl->best)
                                                      : s_bin.best;
             iteration_boundary(P, B, it, n_items, tot_keep, tot_va, tot_commit, n_nodes, accepted, s_bin, best, s_t0);
+#ifdef KP_STAMPS
+            kp_stamps[it & 63][12] = globaltimer();
+#endif
         }
     }
 }
 
-__global__ void __launch_bounds__(KP_SELECT_THREADS, 1024 / KP_SELECT_THREADS) k_select_scatter(KpProblem P, KpBuffers B) {
+// 3 blocks/SM (up to 80 registers): at 4 (64 registers) the committed
+// node's record spilled (forest 4.54 vs 4.61 G/s, TTFS 0.58 vs 0.56 ms)
+#ifndef KP_SCATTER_MINB
+#define KP_SCATTER_MINB (768 / KP_SELECT_THREADS)
+#endif
+__global__ void __launch_bounds__(KP_SELECT_THREADS, KP_SCATTER_MINB) k_select_scatter(KpProblem P, KpBuffers B) {
+    KP_T0;
     pdl_wait();
+    KP_T1;
     pdl_trigger();
+#ifdef KP_STAMPS
+    const uint32_t it_s = B.ctl->iter;
+    KP_STAMP_B0(it_s, 7, kp_t_entry);
+    KP_STAMP_B0(it_s, 8, kp_t_pdl);
+    KP_STAMP_B0(it_s, 9, globaltimer());
+#endif
     scatter_phase(P, B);
 }
 
@@ -1730,6 +1816,16 @@ cudaError_t launch_reintegrate(const KpProblem& P, const KpBuffers& B, const int
 }  // namespace kp
 
 namespace kp {
+// Stamps build: copy the 64 x 16 phase stamps (KP_STAMPS), else an error.
+cudaError_t read_stamps(unsigned long long* out) {
+#ifdef KP_STAMPS
+    return cudaMemcpyFromSymbol(out, kp_stamps, sizeof(kp_stamps));
+#else
+    (void)out;
+    return cudaErrorNotSupported;
+#endif
+}
+
 // Checks build: first failed device invariant (0 = none), cleared on read.
 cudaError_t read_check_code(unsigned int* code) {
 #ifdef KP_CHECKS
