@@ -287,9 +287,9 @@ int kp_get_trace(kp_planner* planner, kp_trace_entry* buf, size_t cap, size_t* l
 int kp_get_stream(kp_planner* planner, void** stream);
 
 /* Diagnostics of a library built with -DKP_STAMPS (scripts/stamps.py): the
- * %globaltimer phase stamps of the last 64 iterations, 64 x 16 uint64 (row =
+ * %globaltimer phase stamps of the last 64 iterations, 64 x 32 uint64 (row =
  * iteration mod 64; columns in kp_kernels.cu).  KP_ERR_CONFIG otherwise. */
-int kp_debug_stamps(kp_planner* planner, uint64_t* out_64x16);
+int kp_debug_stamps(kp_planner* planner, uint64_t* out_64x32);
 
 /* ---- propagation sweep (BASELINE config 5) -------------------------------- */
 

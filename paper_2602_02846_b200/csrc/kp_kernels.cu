@@ -60,11 +60,11 @@ KP_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 KP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Diagnostic build only (-DKP_STAMPS, scripts/stamps.py): %globaltimer stamps
-// of kernel phases per iteration (a ring of 64 iterations x 16 points) — block
+// of kernel phases per iteration (a ring of 64 iterations x 32 points) — block
 // 0's entry / PDL release / control-block arrival and the latest block exit
 // of each kernel, the closing scatter block's ticket and boundary.
 #ifdef KP_STAMPS
-__device__ unsigned long long kp_stamps[64][16];
+__device__ unsigned long long kp_stamps[64][32];
 #define KP_STAMP_B0(it, k, t)                                                        \
     do {                                                                            \
         if (blockIdx.x == 0 && threadIdx.x == 0) kp_stamps[(it) & 63][k] = (t);     \
@@ -584,6 +584,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 len_lo[p] = 0u;
                 len_hi[p] = 0u;
             }
+            KP_STAMP_MAX(it, 16);  // diagnostic build: sampling + parent loads done (latest block)
             // (2) exclusive scan of the sample counts over the block
             uint32_t x = seff;
 #pragma unroll
@@ -685,6 +686,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                 }
             }
             __syncthreads();
+            KP_STAMP_MAX(it, 17);  // diagnostic build: sample checks done (latest block)
             // (4) owner thread: path length, region, admission
 #pragma unroll
             for (uint32_t k = 0; k < IPT; ++k) {
@@ -732,6 +734,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
         if (threadIdx.x == 0) fchunk = gridDim.x + atomicAdd(&ctl->prop_cursor, 1u);
         __syncthreads();
     }
+    KP_STAMP_MAX(it, 18);  // diagnostic build: admissions issued (latest block)
     count_flush(ctl, c, fcnt, lane);
 }
 
@@ -1036,6 +1039,7 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
                 if (a) B.admit_mask[w] = 0u;  // consumed: ready for the next propagate
             }
         }
+        KP_STAMP_MAX(it, 19);  // diagnostic build: prune + commit tests done (latest block)
         const Cnt3 tot = block_sum3(x);
         KP_ASSERT(tile < B.max_tiles, 27);
         if (threadIdx.x == 0) {
@@ -1816,7 +1820,7 @@ cudaError_t launch_reintegrate(const KpProblem& P, const KpBuffers& B, const int
 }  // namespace kp
 
 namespace kp {
-// Stamps build: copy the 64 x 16 phase stamps (KP_STAMPS), else an error.
+// Stamps build: copy the 64 x 32 phase stamps (KP_STAMPS), else an error.
 cudaError_t read_stamps(unsigned long long* out) {
 #ifdef KP_STAMPS
     return cudaMemcpyFromSymbol(out, kp_stamps, sizeof(kp_stamps));
