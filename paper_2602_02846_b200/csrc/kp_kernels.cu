@@ -992,12 +992,16 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
         if (!ly.sparse) {  // one slot per thread; slot elements are warp-aligned
             bool commit = false;
             const uint32_t sl = e - ly.slot0;
-            if (in_slots) {
-                nslot += sl < n_items;
-                if (sl < n_items && ((B.admit_mask[sl >> 5] >> (sl & 31)) & 1u)) {
+            if (in_slots && sl < n_items) {
+                ++nslot;
+                // the slot record is loaded beside its admit bit (one round trip
+                // less; a stale record of an unadmitted slot is never used)
+                const uint32_t aw = B.admit_mask[sl >> 5];
+                const uint32_t va_acc = B.vu_acc[sl], va_reg = B.vu_region[sl];
+                if ((aw >> (sl & 31)) & 1u) {
                     ++nadm;
-                    KP_ASSERT(B.vu_region[sl] < P.n_regions, 25);
-                    commit = B.vu_acc[sl] == B.rc[B.vu_region[sl]];  // Alg. 4 line 3, bit-exact
+                    KP_ASSERT(va_reg < P.n_regions, 25);
+                    commit = va_acc == B.rc[va_reg];  // Alg. 4 line 3, bit-exact
                     x.c = commit;
                 }
             }
@@ -1253,9 +1257,10 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         } else if (el.in_slots) {
             el.w = e - ly.slot0;  // slot (dense) or mask word (sparse)
             if (!ly.sparse) {
-                if (el.w < n_items) {
-                    el.x.c = (B.commit_mask[el.w >> 5] >> (el.w & 31)) & 1u;
-                    el.gm = el.x.c ? (B.goal_mask[el.w >> 5] >> (el.w & 31)) & 1u : 0u;
+                if (el.w < n_items) {  // both mask words in one round trip
+                    const uint32_t cw = B.commit_mask[el.w >> 5], gw = B.goal_mask[el.w >> 5];
+                    el.x.c = (cw >> (el.w & 31)) & 1u;
+                    el.gm = el.x.c & (gw >> (el.w & 31));
                 }
             } else {
                 el.cm = B.commit_mask[el.w];
