@@ -1689,6 +1689,21 @@ static cudaError_t launch_k(Kern kernel, int grid, int block, size_t smem, cudaS
     return cudaLaunchKernelEx(&cfg, kernel, P, B);
 }
 
+// The scatter grid never exceeds what is resident at once (3 blocks/SM at its
+// 80 registers): blocks of a second wave would start only after the first
+// wave's, and a growth-phase iteration with more tiles than blocks measured
+// its tile prefix ~7 µs late; a resident block takes several tiles in turn.
+static int scatter_grid(int grid_sel) {
+    static const int resident = [] {
+        int dev = 0, sms = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_select_scatter, KP_SELECT_THREADS, 0);
+        return std::max(1, sms * occ);
+    }();
+    return std::min(grid_sel, resident);
+}
+
 cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_prop, int grid_sel, cudaStream_t st,
                              int which) {
     const size_t smem = propagate_smem(P);
@@ -1707,7 +1722,7 @@ cudaError_t launch_iteration(const KpProblem& P, const KpBuffers& B, int grid_pr
                        : launch_k(k_select_reduce<false>, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
         if (e != cudaSuccess) return e;
     }
-    if (which & 4) e = launch_k(k_select_scatter, grid_sel, KP_SELECT_THREADS, 0, st, P, B);
+    if (which & 4) e = launch_k(k_select_scatter, scatter_grid(grid_sel), KP_SELECT_THREADS, 0, st, P, B);
     return e;
 }
 

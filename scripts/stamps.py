@@ -34,3 +34,10 @@ nxt = np.median(s[1:, 1] - s[:-1, 1])
 print(f"{scene}: median over {len(s)} iterations, µs relative to propagate's PDL release; iteration period {nxt:.2f} µs")
 for n, v in rows:
     print(f"  {n:22s} {v:8.2f}")
+if len(sys.argv) > 3 and sys.argv[3] == "rows":
+    print("per iteration (µs from propagate's PDL release): P ctl, P sampled, P checks, P exit | R ctl, R prune, R exit | "
+          "S ctl, S prefix, S scan, S writes, S pre-ticket, boundary end | period")
+    for j in range(len(s)):
+        b = s[j, 1]
+        per = s[j + 1, 1] - b if j + 1 < len(s) else float("nan")
+        print(" ".join(f"{s[j, k] - b:6.1f}" for k in (14, 16, 17, 2, 5, 19, 6, 9, 15, 3, 4, 13, 12)), f"| {per:6.1f}")
