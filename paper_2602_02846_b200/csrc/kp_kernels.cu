@@ -973,6 +973,10 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
     const int lane = threadIdx.x & 31;
     uint32_t term = 0, deact = 0, react = 0, hops = 0, nlive = 0, nslot = 0, nadm = 0;
     if (threadIdx.x < 7) s_st[threadIdx.x] = 0;
+#ifdef KP_STAMPS
+    __shared__ unsigned long long s_tmax[2];
+    if (threadIdx.x < 2) s_tmax[threadIdx.x] = 0;
+#endif
     __syncthreads();
     for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint32_t e = tile * KP_SELECT_THREADS + threadIdx.x;
@@ -987,6 +991,9 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
             const uint32_t st = si & 0xFFu;
             x.k = st != KP_ST_TERMINAL;
             x.v = st == KP_ST_ACTIVE;
+#ifdef KP_STAMPS
+            atomicMax(&s_tmax[0], globaltimer());  // latest prune of a live node (block max)
+#endif
         }
         const bool in_slots = e >= ly.slot0 && e < ly.E;
         if (!ly.sparse) {  // one slot per thread; slot elements are warp-aligned
@@ -1043,6 +1050,15 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
                 if (a) B.admit_mask[w] = 0u;  // consumed: ready for the next propagate
             }
         }
+#ifdef KP_STAMPS
+        if (ly.sparse ? (e >= ly.slot0 && e < ly.E) : (e >= ly.slot0 && e - ly.slot0 < n_items))
+            atomicMax(&s_tmax[1], globaltimer());  // latest commit test (block max)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (s_tmax[0]) atomicMax(&kp_stamps[it & 63][20], s_tmax[0]);
+            if (s_tmax[1]) atomicMax(&kp_stamps[it & 63][21], s_tmax[1]);
+        }
+#endif
         KP_STAMP_MAX(it, 19);  // diagnostic build: prune + commit tests done (latest block)
         const Cnt3 tot = block_sum3(x);
         KP_ASSERT(tile < B.max_tiles, 27);

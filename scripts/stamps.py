@@ -25,10 +25,11 @@ s = s[s[:, 0] > 0]
 names = {0: "P entry", 1: "P pdl", 14: "P ctl", 2: "P last exit", 3: "S max first scan done", 4: "S max writes issued",
          5: "R ctl", 6: "R last exit", 7: "S entry", 8: "S pdl", 9: "S ctl", 13: "S last pre-ticket",
          10: "S close pre-ticket", 11: "S close post-ticket", 12: "S boundary end", 15: "S max prefix pass done",
-         16: "P max sampled", 17: "P max checks done", 18: "P max admitted", 19: "R max prune done"}
+         16: "P max sampled", 17: "P max checks done", 18: "P max admitted", 19: "R max prune done",
+         20: "R max live pruned", 21: "R max slot tested"}
 base = s[:, 1]  # propagate PDL release
 rows = []
-for k in (0, 1, 14, 16, 17, 18, 2, 5, 19, 6, 7, 8, 9, 15, 3, 4, 13, 10, 11, 12):
+for k in (0, 1, 14, 16, 17, 18, 2, 5, 20, 21, 19, 6, 7, 8, 9, 15, 3, 4, 13, 10, 11, 12):
     rows.append((names[k], np.median(s[:, k] - base)))
 nxt = np.median(s[1:, 1] - s[:-1, 1])
 print(f"{scene}: median over {len(s)} iterations, µs relative to propagate's PDL release; iteration period {nxt:.2f} µs")
