@@ -2,8 +2,8 @@
 // plus reset/start/debug/trajectory helpers.
 //
 // One iteration (Alg. 1 lines 6-9) = three launches on one
-// stream, captured 8 iterations at a time into a CUDA graph with programmatic
-// dependent launch between the kernels:
+// stream, captured 8 / 32 iterations at a time into CUDA graphs with
+// programmatic dependent launch between the kernels (kp_capi.cpp):
 //
 //   k_propagate<MODEL>   Alg. 2: per V_U slot (frontier
 //                        position x branch) a Philox/SplitMix draw, the
@@ -15,8 +15,10 @@
 //                        bit.  Two paths: step-sorted (a block sorts its chunk
 //                        by step count, a thread per slot; quadcopter rollouts
 //                        split in two passes with compaction) and, for the
-//                        double integrator's one-wave launches, sample-parallel
-//                        (flat_phase: a batch of items flattened into samples).
+//                        double integrator's launches of up to two batches per
+//                        block, sample-parallel (flat_phase: a batch of items
+//                        flattened into 2-sample chunks).  The environment blob
+//                        arrives by one bulk (TMA) copy on an mbarrier.
 //   k_select_reduce      Alg. 3 + the commit test of Alg. 4.
 //                        Element space = [live nodes] ++ [slots, or 32-slot
 //                        mask words when few are admitted].  Live nodes: prune
@@ -31,7 +33,8 @@
 //                        are written to the SoA node store, goal leaves do a
 //                        64-bit atomicMin on (cost bits << 32 | id).  The last
 //                        block closes the iteration: counts, stats, best /
-//                        timeline / TTFS from %globaltimer, termination.
+//                        timeline / TTFS from %globaltimer, termination (its
+//                        inputs prefetched with the block's control-block reads).
 //
 // No kernel waits on another block: cross-block results flow through the
 // "last block" ticket pattern (acq_rel atomic counter), never a spin; the one
