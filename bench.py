@@ -62,18 +62,29 @@ def _peaks():
 # derivative evaluations (+2 per wrapped angle).  sincos recipe = 15.  The
 # double integrator's samples are closed-form: t and t*t, then
 # per position dim u/2 and two FMAs, per velocity dim one FMA; + bounds,
-# distance and cost add as above.
+# distance and cost add as above.  The Dubins airplane's stages (round 2,
+# DESIGN.md §4): 2 stage speeds, 4N accumulate + combine, one slope with two
+# sincos at the step start and two rotated slopes (2 rotations x 4 + 4 each;
+# stage 3 equals stage 2), plus per item the four rotation factors (4 sincos
+# + 5).
 _SINCOS = 15
 OPS_PER_STEP = {
     "double_integrator_4d": 2 + 2 * 4 + 8 + 5 + 1,                               # 24
     "double_integrator_6d": 2 + 3 * 4 + 12 + 7 + 1,                              # 34
-    "dubins_airplane_6d": 3 * 6 + 4 * 6 + 1 + 12 + 7 + 1 + 2 + 4 * (2 * _SINCOS + 4),   # 201
+    "dubins_airplane_6d": 2 + 4 * 6 + 1 + 12 + 7 + 1 + 2 + (2 * _SINCOS + 4) + 2 * 12,   # 107
     "quadcopter_12d": 3 * 12 + 4 * 12 + 1 + 24 + 7 + 1 + 6 + 4 * (3 * _SINCOS + 26),   # 407
 }
 OPS_PER_ITEM = 35      # U conversions + control FMAs, S = ceil(dt/h), region index (3 dims), goal test, acc add
+OPS_PER_ITEM_MODEL = {"dubins_airplane_6d": 4 * _SINCOS + 5}  # the Dubins rotation factors (step_ctx)
 OPS_PER_BOX = 6        # six closed-interval compares
 OPS_PER_SPHERE = 7     # 3 sub + mul + 2 fma + compare
 OPS_PER_INTERP = 4     # j/k + 3 fma
+
+
+def lane_ops(model, d):
+    """Algorithmic FP32 lane-ops of the work counted in a kp_profile (delta) d."""
+    return (d["rk4_steps"] * OPS_PER_STEP[model] + d["items"] * (OPS_PER_ITEM + OPS_PER_ITEM_MODEL.get(model, 0))
+            + d["box_tests"] * OPS_PER_BOX + d["sphere_tests"] * OPS_PER_SPHERE + d["interp_points"] * OPS_PER_INTERP)
 
 
 class ClockSampler:
@@ -474,9 +485,7 @@ def other_configs(args, budget):
                 rows = []
                 for k in (18, 20, 22):
                     ms, one = g.sweep((1 << k) // 32, launches=3)
-                    ops = (one["rk4_steps"] * OPS_PER_STEP[model] + one["items"] * OPS_PER_ITEM
-                           + one["box_tests"] * OPS_PER_BOX + one["sphere_tests"] * OPS_PER_SPHERE
-                           + one["interp_points"] * OPS_PER_INTERP)
+                    ops = lane_ops(model, one)
                     rows.append({"k": k, "items_per_s": one["items"] / (ms * 1e-3),
                                  "frac": ops / (ms * 1e-3) / pk["fp32_lane_ops"]})
             mi = {"double_integrator_6d": 1, "quadcopter_12d": 3}[model]
@@ -507,8 +516,7 @@ def roofline(scenario, pa, pb):
     pk = _peaks()
     model = scenario["problem"]["model"]
     d = {k: pb[k] - pa[k] for k in pb}
-    ops = (d["rk4_steps"] * OPS_PER_STEP[model] + d["items"] * OPS_PER_ITEM + d["box_tests"] * OPS_PER_BOX
-           + d["sphere_tests"] * OPS_PER_SPHERE + d["interp_points"] * OPS_PER_INTERP)
+    ops = lane_ops(model, d)
     n_prop = max(1, d["n_propagate"])
     t_prop = d["t_propagate_s"] / n_prop
     ops_launch = ops / n_prop
@@ -584,9 +592,7 @@ def run_sweep(args, scenario):
             t0 = time.time()
             ms, one = g.sweep(n, launches=launches)
             windows.append((t0, time.time()))
-            ops = (one["rk4_steps"] * OPS_PER_STEP[model] + one["items"] * OPS_PER_ITEM
-                   + one["box_tests"] * OPS_PER_BOX + one["sphere_tests"] * OPS_PER_SPHERE
-                   + one["interp_points"] * OPS_PER_INTERP)
+            ops = lane_ops(model, one)
             rate = ops / (ms * 1e-3)
             rows.append({"k": k, "items": one["items"], "frontier_nodes": n, "ms_per_launch": ms,
                          "items_per_s": one["items"] / (ms * 1e-3), "rk4_steps": one["rk4_steps"],

@@ -136,6 +136,7 @@ struct Faithful64 {
     using Enc = uint64_t;
     static R madd(R a, R b, R c) { return a * b + c; }  // two roundings (-ffp-contract=off)
     static constexpr bool kClosedFormDI = false;         // the reference's RK4 for every model
+    static constexpr bool kRotatedDubins = false;
     static void sincos(R x, R* s, R* c) { *s = std::sin(x); *c = std::cos(x); }
     static Enc encode(R v) { Enc e; std::memcpy(&e, &v, sizeof e); return e; }
     static R decode(Enc e) { R v; std::memcpy(&v, &e, sizeof v); return v; }
@@ -147,6 +148,7 @@ struct Mirror32 {
     using Enc = uint32_t;
     static R madd(R a, R b, R c) { return std::fma(a, b, c); }
     static constexpr bool kClosedFormDI = true;  // device recipe: double integrator in closed form
+    static constexpr bool kRotatedDubins = true;  // device recipe: Dubins stage trigonometry by rotation
     static void sincos(R x, R* s, R* c) { sincos_recipe_f32(x, s, c); }
     static Enc encode(R v) { Enc e; std::memcpy(&e, &v, sizeof e); return e; }
     static R decode(Enc e) { R v; std::memcpy(&v, &e, sizeof v); return v; }
@@ -426,6 +428,49 @@ bool propagate_ode(const ProblemDef& pd, const Consts<P>& k, const Vec<typename 
         const R hk = (s + 1 < S) ? h : dt - R(S - 1) * h;
         if (!(hk > R(0))) break;
         const R half = R(0.5) * hk;
+        if constexpr (P::kRotatedDubins) {
+            if (pd.model == ModelId::Dubins6) {
+                // the device recipe (kp_math.cuh rk4_step<2>): heading and
+                // flight-path rates are the constant controls, so the stage angles'
+                // sines / cosines are those of the step's start rotated by
+                // {sin, cos}(hk/2 u) and {sin, cos}(hk u); stage 3 equals stage 2
+                R rot[8];
+                P::sincos(half * u[0], &rot[0], &rot[1]);
+                P::sincos(hk * u[0], &rot[2], &rot[3]);
+                P::sincos(half * u[1], &rot[4], &rot[5]);
+                P::sincos(hk * u[1], &rot[6], &rot[7]);
+                auto rot2 = [](R s, R c, R rs, R rc, R* so, R* co) {
+                    *so = P::madd(s, rc, c * rs);
+                    *co = P::madd(c, rc, -(s * rs));
+                };
+                auto slope = [&](R sp, R cp, R sg, R cg, R v, Vec<R>& f) {
+                    f.n = n;
+                    const R vc = v * cg;
+                    f[0] = vc * cp; f[1] = vc * sp; f[2] = v * sg;
+                    f[3] = u[0]; f[4] = u[1]; f[5] = u[2];
+                };
+                R sp, cp, sg, cg;
+                P::sincos(x[3], &sp, &cp);
+                P::sincos(x[4], &sg, &cg);
+                slope(sp, cp, sg, cg, x[5], k1);
+                R sp1, cp1, sg1, cg1;
+                rot2(sp, cp, rot[0], rot[1], &sp1, &cp1);
+                rot2(sg, cg, rot[4], rot[5], &sg1, &cg1);
+                slope(sp1, cp1, sg1, cg1, P::madd(half, u[2], x[5]), k2);
+                for (int i = 0; i < n; ++i) k1[i] = P::madd(R(2), k2[i], P::madd(R(2), k2[i], k1[i]));
+                R sp2, cp2, sg2, cg2;
+                rot2(sp, cp, rot[2], rot[3], &sp2, &cp2);
+                rot2(sg, cg, rot[6], rot[7], &sg2, &cg2);
+                slope(sp2, cp2, sg2, cg2, P::madd(hk, u[2], x[5]), k4);
+                const R sixth = hk / R(6);
+                for (int i = 0; i < n; ++i) x[i] = P::madd(sixth, k1[i] + k4[i], x[i]);
+                for (int ad : pd.angle_dims) x[ad] = wrap_angle<P>(x[ad]);
+                for (int i = 0; i < n; ++i)
+                    if (!std::isfinite(x[i])) return false;
+                samples.push_back(x);
+                continue;
+            }
+        }
         // slopes accumulated in production order: acc = ((k1 + 2 k2) + 2 k3) + k4
         // (the device keeps only acc and the current stage live)
         Vec<R>& acc = k1;

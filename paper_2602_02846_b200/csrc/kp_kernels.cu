@@ -1597,9 +1597,11 @@ __global__ void k_reintegrate(KpProblem P, KpBuffers B, const int32_t* chain, ui
     float px = x[0], py = x[1], pz = N >= 3 && MODEL != 0 ? x[2] : 0.0f;
     float x0[N];
     for (int d = 0; d < N; ++d) x0[d] = x[d];
+    float ctx[8];
+    step_ctx<MODEL>(u, P.h, ctx);
     uint32_t w = off[j];
     for (int s = 0; s < S; ++s) {
-        if (advance<MODEL>(P, x0, x, u, dt, S, s, P.h / 6.0f) == 1) break;
+        if (advance<MODEL>(P, x0, x, u, dt, S, s, P.h / 6.0f, ctx) == 1) break;
         for (int d = 0; d < N; ++d) out[static_cast<size_t>(w) * N + d] = x[d];
         ++w;
         const float nx = x[0], ny = x[1], nz = MODEL != 0 ? x[2] : 0.0f;

@@ -219,18 +219,71 @@ KP_DEV void derivative(const KpProblem& P, const float* x, const float* u, float
     }
 }
 
+// Per-segment factors of an RK4 step of length hk.  Dubins
+// airplane: the heading and flight-path rates are the controls u0, u1,
+// constant over a segment, so a step's stage angles are a, a + hk/2 u, a +
+// hk/2 u (stages 2 and 3 alike) and a + hk u; their sines and cosines are
+// those of a rotated by {sin, cos}(hk/2 u) and {sin, cos}(hk u), computed
+// once per segment: ctx = {s, c of hk/2 u0, s, c of hk u0, the same for u1}.
+template <int MODEL>
+KP_DEV void step_ctx(const float* u, float hk, float* ctx) {
+    if constexpr (MODEL == 2) {
+        const float half = 0.5f * hk;
+        sincos_recipe<true>(half * u[0], ctx[0], ctx[1]);
+        sincos_recipe<true>(hk * u[0], ctx[2], ctx[3]);
+        sincos_recipe<true>(half * u[1], ctx[4], ctx[5]);
+        sincos_recipe<true>(hk * u[1], ctx[6], ctx[7]);
+    } else {
+        (void)u; (void)hk; (void)ctx;
+    }
+}
+
+// (s, c) rotated by the angle whose sine / cosine are (rs, rc).
+KP_DEV void rotate_sc(float s, float c, float rs, float rc, float& so, float& co) {
+    so = fmaf(s, rc, c * rs);
+    co = fmaf(c, rc, -(s * rs));
+}
+
+// Dubins airplane slope from its stage trigonometry (derivative<2> layout).
+KP_DEV void dubins_slope(float sp, float cp, float sg, float cg, float v, const float* u, float* f) {
+    const float vc = v * cg;
+    f[0] = vc * cp; f[1] = vc * sp; f[2] = v * sg;
+    f[3] = u[0]; f[4] = u[1]; f[5] = u[2];
+}
+
 // One classical RK4 step with constant control, then angle wrap.
 // `sixth` must equal hk / 6.0f (IEEE division; hoisted by the caller for the
-// full-length steps).  Returns false when a coordinate is non-finite
-// (propagation diverged).
+// full-length steps), ctx = step_ctx(u, hk).  Returns false when a coordinate
+// is non-finite (propagation diverged).
 template <int MODEL>
-KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk, float sixth) {
+KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk, float sixth, const float* ctx) {
     constexpr int N = Model<MODEL>::N;
     // the stage slopes are accumulated as they are produced, acc = k1 + 2 k2 +
     // 2 k3 + k4 in that order: only acc and the current stage stay live (the
     // quadcopter's 12-dim step otherwise holds k1 and k2 across later stages)
     float k[N], acc[N], t[N];
     const float half = 0.5f * hk;
+    if constexpr (MODEL == 2) {
+        // stage trigonometry by rotation (step_ctx); the stage speeds are
+        // x5 + hk/2 u2 (stages 2, 3) and x5 + hk u2, and positions do not enter
+        // the slope, so stage 3 equals stage 2
+        (void)t;
+        float sp, cp, sg, cg;
+        sincos_recipe(x[3], sp, cp);
+        sincos_recipe<true>(x[4], sg, cg);
+        dubins_slope(sp, cp, sg, cg, x[5], u, acc);
+        float sp1, cp1, sg1, cg1;
+        rotate_sc(sp, cp, ctx[0], ctx[1], sp1, cp1);
+        rotate_sc(sg, cg, ctx[4], ctx[5], sg1, cg1);
+        dubins_slope(sp1, cp1, sg1, cg1, fmaf(half, u[2], x[5]), u, k);
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[i] = fmaf(2.0f, k[i], fmaf(2.0f, k[i], acc[i]));  // + 2 k2 + 2 k3
+        float sp2, cp2, sg2, cg2;
+        rotate_sc(sp, cp, ctx[2], ctx[3], sp2, cp2);
+        rotate_sc(sg, cg, ctx[6], ctx[7], sg2, cg2);
+        dubins_slope(sp2, cp2, sg2, cg2, fmaf(hk, u[2], x[5]), u, k);
+    } else {
+    (void)ctx;
     derivative<MODEL>(P, x, u, acc);
 #pragma unroll
     for (int i = 0; i < N; ++i) t[i] = fmaf(half, acc[i], x[i]);
@@ -247,6 +300,7 @@ KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk, flo
         acc[i] = fmaf(2.0f, k[i], acc[i]);
     }
     derivative<MODEL>(P, t, u, k);
+    }
 #pragma unroll
     for (int i = 0; i < N; ++i) x[i] = fmaf(sixth, acc[i] + k[i], x[i]);
     if constexpr (Model<MODEL>::NA > 0) {
@@ -270,7 +324,9 @@ KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk, flo
 
 template <int MODEL>
 KP_DEV bool rk4_step(const KpProblem& P, float* x, const float* u, float hk) {
-    return rk4_step<MODEL>(P, x, u, hk, hk / 6.0f);
+    float ctx[8];
+    step_ctx<MODEL>(u, hk, ctx);
+    return rk4_step<MODEL>(P, x, u, hk, hk / 6.0f, ctx);
 }
 
 // Double integrator in closed form: RK4 with constant control is exact on it
@@ -527,7 +583,8 @@ KP_DEV bool segment_hit(const KpProblem& P, const Env& E, float px, float py, fl
 // of x (h6 = h / 6).  Returns 0, 1 when the shortened last step is empty
 // (dt - (S-1) h <= 0: the rollout ends at sample S - 1), 2 when diverged.
 template <int MODEL>
-KP_DEV int advance(const KpProblem& P, const float* x0, float* x, const float* u, float dt, int S, int s, float h6) {
+KP_DEV int advance(const KpProblem& P, const float* x0, float* x, const float* u, float dt, int S, int s, float h6,
+                   const float* ctx) {
     if constexpr (closed_form<MODEL>()) {
         float t = static_cast<float>(s + 1) * P.h;
         if (s + 1 == S) {
@@ -550,8 +607,11 @@ KP_DEV int advance(const KpProblem& P, const float* x0, float* x, const float* u
             if (!(hk > 0.0f)) return 1;
             // IEEE div.rn (== hk / 6.0f); volatile so it is not if-converted into every step
             asm volatile("div.rn.f32 %0, %1, %2;" : "=f"(sixth) : "f"(hk), "f"(6.0f));
+            float ctx_last[8];  // the per-segment factors are for full steps
+            step_ctx<MODEL>(u, hk, ctx_last);
+            return rk4_step<MODEL>(P, x, u, hk, sixth, ctx_last) ? 0 : 2;
         }
-        return rk4_step<MODEL>(P, x, u, hk, sixth) ? 0 : 2;
+        return rk4_step<MODEL>(P, x, u, hk, sixth, ctx) ? 0 : 2;
     }
 }
 
@@ -593,6 +653,8 @@ KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const flo
 #pragma unroll
     for (int i = 0; i < N; ++i) x0[i] = x[i];
     long long fx = 0;  // closed form: fixed-point path length
+    float ctx[8];      // per-segment step factors (step_ctx)
+    step_ctx<MODEL>(u, P.h, ctx);
     bool vel = true;   // check the velocity dims at every sample
     if constexpr (closed_form<MODEL>()) {
         if (!P.check_finite) {
@@ -601,7 +663,7 @@ KP_DEV int integrate_steps(const KpProblem& P, const Env& E, float* x, const flo
         }
     }
     for (int s = s0; s < s1; ++s) {
-        const int st = advance<MODEL>(P, x0, x, u, dt, S, s, h6);
+        const int st = advance<MODEL>(P, x0, x, u, dt, S, s, h6, ctx);
         if (st == 1) break;
         if (st == 2) return 2;
         o.steps += 1;
