@@ -156,12 +156,16 @@ KP_DEV void env_wait() {
 // the register-heavy quadcopter (3 blocks/SM); chunks of at most 1024 slots.
 template <int MODEL>
 struct PropCfg {
-    static constexpr int T = MODEL == 3 ? 256 : 512;  // threads per block
-    static constexpr int MAXG = 1024 / T;             // slot rounds per chunk
 #ifndef KP_QUAD_MINB
 #define KP_QUAD_MINB 3
 #endif
-    static constexpr int MIN_BLOCKS = MODEL == 3 ? KP_QUAD_MINB : 2;
+#ifndef KP_DUBINS_T
+#define KP_DUBINS_T 512
+#define KP_DUBINS_MINB 2
+#endif
+    static constexpr int T = MODEL == 3 ? 256 : (MODEL == 2 ? KP_DUBINS_T : 512);  // threads per block
+    static constexpr int MAXG = 1024 / T;                                          // slot rounds per chunk
+    static constexpr int MIN_BLOCKS = MODEL == 3 ? KP_QUAD_MINB : (MODEL == 2 ? KP_DUBINS_MINB : 2);
     // Steps of the first pass of a split rollout (0: never split).  Only the
     // quadcopter splits: ~55 % of its items stop early (invalid), and a first
     // pass of 8 steps cuts its warp-steps by ~22 % (scripts/split_sim.py); for
@@ -175,7 +179,6 @@ struct PropCfg {
 #endif
 };
 
-int prop_threads(int model) { return model == 3 ? PropCfg<3>::T : PropCfg<1>::T; }
 #define KP_SORT_BUCKETS 64
 
 // the split rollouts' per-group masks (32 entries) and the per-block scratch
