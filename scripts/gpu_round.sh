@@ -21,6 +21,10 @@ timeout 600 python bench.py --batch 64 --lanes 8 > $OUT/bench_batch.json 2> $OUT
 python scripts/trace_gpu.py forest_di6 > $OUT/trace_forest_di6.txt 2>&1
 python scripts/trace_gpu.py building_quad12 1.0 > $OUT/trace_building_quad12.txt 2>&1
 python scripts/trace_gpu.py narrow_dubins6 > $OUT/trace_narrow_dubins6.txt 2>&1
+# launch list of the bench command itself (first 400 launches: the warm-up queries; same command first without ncu)
+BCMD="python bench.py --steps 2 --warmup 3 --no-extras --no-cpu-baseline --dist-seeds 0"
+timeout 600 $BCMD > $OUT/plain_bench_short.json 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_bench.csv $BCMD > $OUT/ncu_bench.log 2>&1
 # launch list of a fixed-iteration query (the same command first without ncu)
 PCMD="python scripts/prof_run.py forest_di6 60"
 timeout 300 $PCMD > $OUT/plain_launch.log 2>&1 && \
@@ -36,6 +40,9 @@ done
 timeout 300 python scripts/prof_sweep.py building_quad12 22 > $OUT/plain_sweep.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_propagate -s 2 -c 1 \
    -o $OUT/prop_sweep_building_quad12 -f python scripts/prof_sweep.py building_quad12 22 > $OUT/ncu_sweep.log 2>&1
+timeout 300 python scripts/prof_sweep.py narrow_dubins6 22 > $OUT/plain_sweep_dubins.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_propagate -s 2 -c 1 \
+   -o $OUT/prop_sweep_narrow_dubins6 -f python scripts/prof_sweep.py narrow_dubins6 22 > $OUT/ncu_sweep_dubins.log 2>&1
 timeout 300 python scripts/prof_run.py forest_di6 40 > /dev/null 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_select -s 74 -c 2 \
    -o $OUT/sel_forest_di6 -f python scripts/prof_run.py forest_di6 40 > $OUT/ncu_sel.log 2>&1
