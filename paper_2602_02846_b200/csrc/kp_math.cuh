@@ -118,12 +118,12 @@ KP_DEV void sincos_poly(float r, float& s, float& c) {  // |r| <= pi/4
 
 // SMALL: an angle whose state bounds keep it inside (-pi/4, pi/4) (the
 // quadcopter's roll and pitch, |phi|, |theta| <= 0.6; the airplane's flight
-// path angle, |gamma| <= 0.5).  When |x * 2/pi| < 1/2 for every active lane,
-// j = 0, r == x exactly (fma(-0, c, x) == x) and there is no quadrant fix-up:
-// the same bits as the general path without its reduction and select
-// instructions.  The test is a warp vote so the branch never diverges (a
-// divergent branch runs both paths); headings (psi) always take the general
-// path.
+// path angle, |gamma| <= 0.5, and the per-segment Dubins shifts).  When
+// |x * 2/pi| < 1/2, j = 0, r == x exactly (fma(-0, c, x) == x) and there is no
+// quadrant fix-up: the same bits as the general path without its reduction and
+// select instructions.  A plain per-lane test: for these angles it is
+// warp-uniform in practice (a warp vote made it slower); headings (psi) always
+// take the general path, where a divergent branch would run both.
 template <bool SMALL = false>
 KP_DEV void sincos_recipe(float x, float& s_out, float& c_out) {
     if constexpr (SMALL) {
@@ -166,13 +166,11 @@ KP_DEV float wrap_angle(float a) {
 // for both — the fast path when both have j = 0, else the general path for
 // both (same bits either way).
 KP_DEV void sincos2_small(float a, float b, float& sa, float& ca, float& sb, float& cb) {
-#ifndef KP_NO_SINCOS_FAST
     if (fmaxf(fabsf(a * 0x1.45f306p-1f), fabsf(b * 0x1.45f306p-1f)) < 0.5f) {
         sincos_poly(a, sa, ca);
         sincos_poly(b, sb, cb);
         return;
     }
-#endif
     sincos_recipe(a, sa, ca);
     sincos_recipe(b, sb, cb);
 }
@@ -192,6 +190,8 @@ KP_DEV void derivative(const KpProblem& P, const float* x, const float* u, float
     } else if constexpr (MODEL == 1) {
         f[0] = x[3]; f[1] = x[4]; f[2] = x[5]; f[3] = u[0]; f[4] = u[1]; f[5] = u[2];
     } else if constexpr (MODEL == 2) {
+        // (rk4_step evaluates this slope through dubins_slope, with the stage
+        // trigonometry rotated from the step's start: DESIGN.md §4)
         float sp, cp, sg, cg;
         sincos_recipe(x[3], sp, cp);
         sincos_recipe<true>(x[4], sg, cg);
