@@ -202,6 +202,17 @@ def cpu_planner_run(scenario, seed, budget_s, workers, stop_first, max_iteration
     return r
 
 
+def query_config(args, scenario, ws):
+    """`config` of the default (one query per step) workload, shared by both arms
+    so the reference line names the same workload as ours."""
+    return {"workload": f"{args.config}: one seeded query per step, {args.budget_ms:g} ms budget "
+                        "(Alg. 1 until t_max), replicas across ranks",
+            "budget_ms": args.budget_ms, "seeds_rank0": [args.seed_base, args.seed_base + args.steps - 1],
+            "lambda": scenario["planner"]["lambda"], "capacity": scenario["planner"]["capacity"],
+            "regions": _regions(scenario), "l2": "flushed before every step (256 MiB write)",
+            "parallelism": f"replicas x{ws}"}
+
+
 def run_reference(args, scenario):
     ws, rank, _ = _dist()
     if rank != 0:
@@ -223,8 +234,9 @@ def run_reference(args, scenario):
     line = {
         "impl": "reference", "metric": "node propagations/sec", "value": value, "unit": "propagations/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "budget_ms": args.budget_ms, "seeds": [args.seed_base, args.seed_base + args.steps - 1]},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (pinned scene geometry, seeded queries)",
+        "config": query_config(args, scenario, ws),
         "metrics": {"ms_to_first_solution_median": _median(ttfs), "solution_cost_at_budget_median": _median(costs),
                     "success_rate": found / args.steps, "node_propagations_per_sec": value},
         "cpu_baseline": {"value": value, "unit": "propagations/s", "cores": cores, "kind": "port",
@@ -396,12 +408,7 @@ def run_b200(args, scenario):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / len(seeds),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (pinned scene geometry, seeded queries)",
-            "config": {"workload": f"{args.config}: one seeded query per step, {args.budget_ms:g} ms budget "
-                                   "(Alg. 1 until t_max), replicas across ranks",
-                       "budget_ms": args.budget_ms, "seeds_rank0": [seeds[0], seeds[-1]],
-                       "lambda": scenario["planner"]["lambda"], "capacity": scenario["planner"]["capacity"],
-                       "regions": _regions(scenario), "l2": "flushed before every step (256 MiB write)",
-                       "parallelism": f"replicas x{ws}"},
+            "config": query_config(args, scenario, ws),
             "metrics": {
                 "ms_to_first_solution_median": _median(ttfs),
                 "ms_to_first_solution_p25_p75": _quart(ttfs),
