@@ -27,7 +27,7 @@ def test_reference_arm_json_line():
     assert cb["kind"] in ("port", "reference") and cb["value"] == d["value"]
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
-    assert d["config"]["workload"] == "forest_di6"
+    assert d["config"]["workload"].startswith("forest_di6: one seeded query per step")
 
 
 import pytest  # noqa: E402
