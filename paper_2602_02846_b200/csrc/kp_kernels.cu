@@ -672,16 +672,29 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
                     }
                     long long run = 0;
                     bool ok = true;
-                    for (int s = s0; s <= s1; ++s) {
-                        float xs[N];
-                        di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
-                        float d;
-                        if (!check_sample<MODEL>(P, E, xs, px, py, pz, d, c)) {
-                            ok = false;
-                            break;
+                    if constexpr (K == 2) {
+                        // both samples of a chunk checked (no exit between them): two
+                        // independent sample computations for the scheduler (+0.5 %)
+                        float xa[N], xb[N];
+                        di_sample<MODEL>(x0, u, (s0 == S) ? dt : static_cast<float>(s0) * P.h, xa);
+                        const bool two = s1 > s0;
+                        di_sample<MODEL>(x0, u, (s0 + 1 == S) ? dt : static_cast<float>(s0 + 1) * P.h, xb);
+                        float da, db = 0.0f;
+                        ok = check_sample<MODEL>(P, E, xa, px, py, pz, da, c);
+                        if (two) ok = check_sample<MODEL>(P, E, xb, xa[0], xa[1], TWO_D ? 0.0f : xa[2], db, c) && ok;
+                        run = len_fixed(da) + (two ? len_fixed(db) : 0ll);
+                    } else {
+                        for (int s = s0; s <= s1; ++s) {
+                            float xs[N];
+                            di_sample<MODEL>(x0, u, (s == S) ? dt : static_cast<float>(s) * P.h, xs);
+                            float d;
+                            if (!check_sample<MODEL>(P, E, xs, px, py, pz, d, c)) {
+                                ok = false;
+                                break;
+                            }
+                            run += len_fixed(d);
+                            px = xs[0]; py = xs[1]; pz = TWO_D ? 0.0f : xs[2];
                         }
-                        run += len_fixed(d);
-                        px = xs[0]; py = xs[1]; pz = TWO_D ? 0.0f : xs[2];
                     }
                     if (!ok) {
                         bad[pi] = 1u;
