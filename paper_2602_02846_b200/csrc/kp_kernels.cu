@@ -165,7 +165,10 @@ struct PropCfg {
 #endif
     static constexpr int T = MODEL == 3 ? 256 : (MODEL == 2 ? KP_DUBINS_T : 512);  // threads per block
     static constexpr int MAXG = 1024 / T;                                          // slot rounds per chunk
-    static constexpr int MIN_BLOCKS = MODEL == 3 ? KP_QUAD_MINB : (MODEL == 2 ? KP_DUBINS_MINB : 2);
+#ifndef KP_DI_MINB
+#define KP_DI_MINB 2
+#endif
+    static constexpr int MIN_BLOCKS = MODEL == 3 ? KP_QUAD_MINB : (MODEL == 2 ? KP_DUBINS_MINB : KP_DI_MINB);
     // Steps of the first pass of a split rollout (0: never split).  Only the
     // quadcopter splits: ~55 % of its items stop early (invalid), and a first
     // pass of 8 steps cuts its warp-steps by ~22 % (scripts/split_sim.py); for
