@@ -1652,6 +1652,12 @@ size_t propagate_smem(const KpProblem& P) { return P.prop_smem; }
 // under PDL).  A sample-parallel batch holds KP_FLAT_ITEMS item records,
 // sample offsets, invalid flags and fixed-point path lengths.  KP_FLAT=0
 // turns the sample-parallel path off.
+#ifndef KP_FLAT_SMEM_KB
+#define KP_FLAT_SMEM_KB 96  // propagate's shared memory with the sample-parallel arrays (2 blocks/SM)
+#endif
+#ifndef KP_FLAT_BATCHES
+#define KP_FLAT_BATCHES 2u  // largest sample-parallel launch: batches per block of the grid
+#endif
 void plan_propagate_smem(KpProblem& P) {
     auto pad16 = [](size_t b) { return (b + 15) & ~static_cast<size_t>(15); };
     size_t seq = 0;
@@ -1677,7 +1683,7 @@ void plan_propagate_smem(KpProblem& P) {
         // chunk -> item index
         const size_t idxb = pad16(static_cast<size_t>(nb) * ((smax + KP_FLAT_K - 1) / KP_FLAT_K) * 2);
         const size_t flat = rec + offs + badb + lenb + idxb;
-        if (base + flat <= 96 * 1024) {
+        if (base + flat <= KP_FLAT_SMEM_KB * 1024) {
             P.flat_on = 1;
             P.flat_nb = nb;
             P.flat_rec = static_cast<uint32_t>(base);
@@ -1702,7 +1708,7 @@ void set_flat_limit(KpProblem& P, int grid_prop) {
     if (!P.flat_on) return;
     const char* fm = std::getenv("KP_FLAT_MAX");
     P.flat_max = fm ? static_cast<uint32_t>(std::strtoul(fm, nullptr, 10))
-                    : 2u * P.flat_nb * static_cast<uint32_t>(grid_prop);
+                    : KP_FLAT_BATCHES * P.flat_nb * static_cast<uint32_t>(grid_prop);
 }
 
 static bool pdl_enabled() {

@@ -1,6 +1,7 @@
 """Phase timeline of steady-state iterations from a -DKP_STAMPS build
 (make -B paper_2602_02846_b200/lib/libkinoplan_b200.so NVFLAGS="... -DKP_STAMPS").
-python scripts/stamps.py SCENE [BUDGET_S]   -> mean µs of each phase over the last 64 iterations"""
+python scripts/stamps.py SCENE [BUDGET_S | iN] [rows]   -> median µs of each phase over the last 64
+iterations (iN: stop after N iterations, e.g. i20 for the growth phase; rows: one line per iteration)"""
 import ctypes as C
 import sys
 
@@ -10,10 +11,13 @@ sys.path.insert(0, ".")
 from paper_2602_02846_b200 import Planner, scenarios  # noqa: E402
 
 scene = sys.argv[1] if len(sys.argv) > 1 else "forest_di6"
-budget = float(sys.argv[2]) if len(sys.argv) > 2 else 0.1
+arg = sys.argv[2] if len(sys.argv) > 2 else "0.1"
 with Planner(scenarios.load(scene), seed=1000) as g:
     g.reset(1000)
-    g.solve(budget)
+    if arg.startswith("i"):
+        g.solve(0.0, int(arg[1:]))
+    else:
+        g.solve(float(arg))
     buf = (C.c_uint64 * (64 * 32))()
     rc = g._lib.kp_debug_stamps(g._h, buf)
     if rc != 0:
