@@ -690,7 +690,7 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the other-config summaries")
     ap.add_argument("--sweep", action="store_true", help="BASELINE config 5: propagate throughput sweep")
     ap.add_argument("--batch", type=int, default=0, help="BASELINE config 4: number of queries in the batch")
-    ap.add_argument("--lanes", type=int, default=16, help="concurrent planner lanes per GPU (--batch)")
+    ap.add_argument("--lanes", type=int, default=8, help="concurrent planner lanes per GPU (--batch; 8 measured best)")
     args = ap.parse_args()
     from paper_2602_02846_b200 import scenarios
 
