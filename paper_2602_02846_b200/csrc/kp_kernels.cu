@@ -1828,7 +1828,8 @@ cudaError_t launch_debug_propagate(const KpProblem& P, const KpBuffers& B, uint3
     return cudaGetLastError();
 }
 
-// Sweep support: frontier = nodes 0..n-1, iteration counter fixed, region
+// Sweep support: frontier = nodes 0..n-1 (the store's first n nodes, so
+// kp_get_nodes returns the synthetic states), iteration counter fixed, region
 // table +inf, counters cleared (one launch = n * lambda work items).
 __global__ void k_sweep_prepare(KpProblem P, KpBuffers B, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1843,6 +1844,7 @@ __global__ void k_sweep_prepare(KpProblem P, KpBuffers B, uint32_t n) {
         c->done = 0;
         c->iter = 0;
         c->n_va = n;
+        c->n_nodes = n;
         c->n_items = n * static_cast<uint32_t>(P.lambda);
         c->prop_cursor = 0;
         c->n_adm_iter = 0;

@@ -353,3 +353,51 @@ def test_angle_wrap_all_angles_at_once():
         for r in range(len(ps)):
             ps[r, d] = [pi, -np.nextafter(pi, np.float32(0)), np.float32(3.1), np.float32(-3.1)][r % 4]
         _item_parity(s, ps, seed=29)
+
+
+def _oracle_table(s, seed, states, lam, n_regions, workers=8):
+    """Per-region minimum of the accumulated-cost bits over the valid items of
+    one propagate launch over the frontier `states` (iteration 0, parent cost
+    0, items node-major: node k, branch b), from the oracle's fp32
+    restatement, in threads (ctypes releases the GIL), one oracle per chunk."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    n = states.shape[0]
+    step = max(1, (n + 4 * workers - 1) // (4 * workers))
+
+    def part(lo):
+        hi = min(n, lo + step)
+        k = (hi - lo) * lam
+        ids = np.repeat(np.arange(lo, hi, dtype=np.uint32), lam)
+        brs = np.tile(np.arange(lam, dtype=np.uint32), hi - lo)
+        ps = np.repeat(states[lo:hi].astype(np.float64), lam, axis=0)
+        r = kpo.Oracle(s, kpo.MIRROR32, seed=seed).propagate_items(ps, np.zeros(k), ids, brs, 0)
+        v = r["valid"] == 1
+        t = np.full(n_regions, 0x7F800000, np.uint32)
+        np.minimum.at(t, r["region"][v], r["acc"][v].astype(np.float32).view(np.uint32))
+        return t, int(v.sum())
+
+    with ThreadPoolExecutor(workers) as ex:
+        parts = list(ex.map(part, range(0, n, step)))
+    return np.minimum.reduce([p[0] for p in parts]), sum(p[1] for p in parts)
+
+
+@pytest.mark.parametrize("scene,k", [("building_quad12", 22), ("forest_di6", 22), ("narrow_dubins6", 20)])
+def test_sweep_full_size_region_table(scene, k):
+    """BASELINE config 5 at its full size: one propagate launch over 2^k work
+    items of a synthetic frontier (step-sorted path, many chunks per block).
+    The region table it leaves is the per-region minimum of the valid items'
+    accumulated costs — order-independent, so it must equal the oracle's over
+    every item, bit for bit."""
+    s = scenarios.load(scene, capacity=1 << 22, max_slots=1 << 23)
+    lam = int(s["planner"]["lambda"])
+    n = (1 << k) // lam
+    with Planner(s, seed=5) as g:
+        g.sweep(n, launches=1)
+        states = g.nodes()["state"]
+        table = g.region_table()
+    assert states.shape[0] == n
+    want, n_valid = _oracle_table(s, 5, states, lam, table.shape[0])
+    assert n_valid > 0
+    assert (want != 0x7F800000).sum() > 100
+    np.testing.assert_array_equal(table, want)
