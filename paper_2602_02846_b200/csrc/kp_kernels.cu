@@ -37,7 +37,7 @@
 //                        inputs prefetched with the block's control-block reads).
 //
 // No kernel waits on another block: cross-block results flow through the
-// "last block" ticket pattern (acq_rel atomic counter), never a spin; the one
+// "last block" ticket pattern (an atomic counter), never a spin; the one
 // in-block wait is the split rollouts' second pass behind a block barrier.
 #include <cuda_runtime.h>
 #include <stdint.h>
