@@ -42,7 +42,7 @@ void set_flat_limit(KpProblem& P, int grid_prop);
 int propagate_occupancy(const KpProblem& P);
 cudaError_t launch_reset(const KpProblem& P, const KpBuffers& B, unsigned long long seed, cudaStream_t st);
 cudaError_t launch_start(const KpBuffers& B, unsigned long long budget_ns, uint32_t max_iters, uint32_t stop_first,
-                         cudaStream_t st);
+                         uint32_t seq, cudaStream_t st);
 cudaError_t launch_debug_propagate(const KpProblem& P, const KpBuffers& B, uint32_t n, const float* ps,
                                    const float* pacc, const uint32_t* ids, const uint32_t* brs, uint32_t it,
                                    uint8_t* valid, float* xs, float* us, float* dts, float* accs, uint32_t* regs,
@@ -102,6 +102,7 @@ struct kp_planner {
     cudaGraphExec_t graph = nullptr;       // KP_GRAPH_ITERS iterations
     cudaGraphExec_t graph_head = nullptr;  // KP_GRAPH_HEAD iterations: a solve's first launches
     uint32_t* host_done = nullptr;  // pinned, mapped
+    uint32_t solve_seq = 0;         // number of the current solve (the device writes it to host_done when done)
     std::vector<void*> allocs;
     std::string err;
     KpCtl ctl{};  // host copy after the last solve
@@ -539,6 +540,9 @@ void fetch_ctl(kp_planner* pl, bool after_done = false) {
         cuda_check(cudaStreamSynchronize(st), "ctl timeline sync");
     }
     std::memcpy(&pl->ctl, pl->h_ctl, head + std::max(len, win) * sizeof(KpTimeline));
+    // the last boundary's best-solution bookkeeping, which the device does in
+    // the next propagate (none runs after the solve stopped): the same entry
+    goal_bookkeeping(pl->ctl);
     pl->last_fetch_bytes = head + std::max(len, win) * sizeof(KpTimeline);
     pl->ctl_valid = true;
     check_invariants();
@@ -849,7 +853,10 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
         if (mi > 0xFFFFFFF0ull) throw KpError(KP_ERR_CONFIG, "max_iterations too large");
         const unsigned long long budget_ns = budget > 0 ? static_cast<unsigned long long>(budget * 1e9) : 0ull;
         *pl->host_done = 0;
-        cuda_check(kp::launch_start(pl->B, budget_ns, static_cast<uint32_t>(mi), stop_first ? 1u : 0u, pl->stream),
+        if (++pl->solve_seq == 0) pl->solve_seq = 1;
+        const uint32_t seq = pl->solve_seq;
+        cuda_check(kp::launch_start(pl->B, budget_ns, static_cast<uint32_t>(mi), stop_first ? 1u : 0u, seq,
+                                    pl->stream),
                    "start");
         pl->kernel_launches += 1;
         // host watchdog: the device stops itself at the budget; this only
@@ -860,7 +867,7 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
         volatile uint32_t* done = pl->host_done;
         if (pl->profiling) {
             // per-kernel CUDA-event timing, one iteration at a time
-            while (!*done) {
+            while (*done != seq) {
                 for (int k = 0; k < 3; ++k) {
                     cuda_check(cudaEventRecord(pl->ev[0], pl->stream), "event");
                     cuda_check(kp::launch_iteration(pl->P, pl->B, pl->grid_prop, pl->grid_sel, pl->stream, 1 << k), "iter");
@@ -879,17 +886,17 @@ int kp_solve(kp_planner* pl, double budget_s, uint64_t max_iterations, kp_result
             // raises the mapped done word
             cudaEvent_t inflight[2] = {pl->ev[2], pl->ev[3]};
             int n_launched = 0;
-            while (!*done) {
+            while (*done != seq) {
                 if (n_launched >= 2) {
                     cudaEvent_t e = inflight[n_launched & 1];  // recorded two launches ago
                     for (;;) {
-                        if (*done) break;
+                        if (*done == seq) break;
                         const cudaError_t q = cudaEventQuery(e);
                         if (q == cudaSuccess) break;
                         if (q != cudaErrorNotReady) cuda_check(q, "graph execution");
                         if (wall() > watchdog) throw KpError(KP_ERR_CUDA, "solve watchdog expired");
                     }
-                    if (*done) break;
+                    if (*done == seq) break;
                 }
                 launch_graph(pl, n_launched);
                 cuda_check(cudaEventRecord(inflight[n_launched & 1], pl->stream), "event");
@@ -1080,14 +1087,15 @@ int kp_batch_solve(kp_batch* b, const uint64_t* seeds, size_t k, double budget_s
                     L.q = next++;
                     reset_async(pl, seeds[L.q]);
                     *pl->host_done = 0;
+                    if (++pl->solve_seq == 0) pl->solve_seq = 1;
                     cuda_check(kp::launch_start(pl->B, budget_ns, static_cast<uint32_t>(mi), stop_first ? 1u : 0u,
-                                                pl->stream), "start");
+                                                pl->solve_seq, pl->stream), "start");
                     pl->kernel_launches += 1;
                     L.launched = 0;
                     L.st = RUNNING;
                 }
                 if (L.st == RUNNING) {
-                    if (*pl->host_done) {
+                    if (*pl->host_done == pl->solve_seq) {
                         cuda_check(cudaMemcpyAsync(pl->h_ctl, pl->B.ctl, sizeof(KpCtl), cudaMemcpyDeviceToHost,
                                                    pl->stream), "ctl D2H");
                         cuda_check(cudaEventRecord(pl->ev[0], pl->stream), "event");
@@ -1107,6 +1115,7 @@ int kp_batch_solve(kp_batch* b, const uint64_t* seeds, size_t k, double budget_s
                     if (q == cudaErrorNotReady) continue;
                     cuda_check(q, "batch fetch");
                     std::memcpy(&pl->ctl, pl->h_ctl, sizeof(KpCtl));
+                    goal_bookkeeping(pl->ctl);  // the last boundary's (fetch_ctl)
                     pl->ctl_valid = true;
                     if (pl->ctl.error == 8) throw KpError(KP_ERR_SLOT_OVERFLOW, "lambda*|V_A| exceeded max_slots");
                     fill_result(pl, &results[L.q]);

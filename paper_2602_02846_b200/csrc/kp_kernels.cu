@@ -206,9 +206,29 @@ struct PropSmem {
     uint32_t cnt[6];
 };
 
+// The control-block fields every propagate block reads, in one round trip.
+struct PropCtl {
+    uint32_t done, n_items, it, split, stop_first, seq;
+    unsigned long long seed, best, tl_best;
+};
+
+KP_DEV PropCtl load_prop_ctl(const KpCtl* ctl) {
+    PropCtl c;
+    c.done = ctl->done;
+    c.n_items = ctl->n_items;
+    c.it = ctl->iter;
+    c.split = ctl->split;
+    c.stop_first = ctl->stop_first;
+    c.seq = ctl->solve_seq;
+    c.seed = ctl->seed;
+    c.best = ctl->best;
+    c.tl_best = ctl->tl_best;
+    return c;
+}
+
 // Work counters of a propagate launch: warp-aggregated (one REDUX per
 // counter), then block-aggregated, then one atomic per counter and block.
-KP_DEV void count_flush(KpCtl* ctl, uint32_t* c, uint32_t* cnt, int lane) {
+KP_DEV void count_flush(KpCtl* ctl, uint32_t* c, uint32_t* cnt, int lane, uint32_t it) {
 #pragma unroll
     for (int k = 0; k < 6; ++k) c[k] = __reduce_add_sync(0xFFFFFFFFu, c[k]);
     if (lane == 0) {
@@ -224,7 +244,7 @@ KP_DEV void count_flush(KpCtl* ctl, uint32_t* c, uint32_t* cnt, int lane) {
         }
         if (cnt[1]) {
             atomicAdd(&ctl->stats.admitted, static_cast<unsigned long long>(cnt[1]));
-            atomicAdd(&ctl->n_adm_iter, cnt[1]);
+            atomicAdd(&ctl->n_adm_p[it & 1], cnt[1]);
         }
         if (cnt[2]) atomicAdd(&ctl->stats.rk4_steps, static_cast<unsigned long long>(cnt[2]));
         if (cnt[3]) atomicAdd(&ctl->stats.interp_points, static_cast<unsigned long long>(cnt[3]));
@@ -234,16 +254,16 @@ KP_DEV void count_flush(KpCtl* ctl, uint32_t* c, uint32_t* cnt, int lane) {
 }
 
 template <int MODEL>
-KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MODEL>& sh, const Env& E) {
+KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MODEL>& sh, const Env& E,
+                            const PropCtl& pc) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
     constexpr uint32_t KP_PROP_THREADS = PropCfg<MODEL>::T;
     constexpr uint32_t KP_PROP_MAXG = PropCfg<MODEL>::MAXG;
     KpCtl* ctl = B.ctl;
-    // every control-block read up front: one round trip, not one per early exit
-    const uint32_t done = ctl->done, n_items = ctl->n_items, it = ctl->iter, split_on = ctl->split;
-    const unsigned long long seed = ctl->seed;
-    if (done) return;
+    // the control block was read once by the kernel (PropCtl)
+    const uint32_t n_items = pc.n_items, it = pc.it, split_on = pc.split;
+    const unsigned long long seed = pc.seed;
     if (threadIdx.x < 6) sh.cnt[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
     // Chunk of slots per block: one block width while the launch fits in one
@@ -447,7 +467,7 @@ KP_DEV void propagate_phase(const KpProblem& P, const KpBuffers& B, PropSmem<MOD
         if (threadIdx.x == 0) sh.chunk = gridDim.x + atomicAdd(&ctl->prop_cursor, 1u);
         __syncthreads();
     }
-    count_flush(ctl, c, sh.cnt, lane);
+    count_flush(ctl, c, sh.cnt, lane, it);
 }
 
 // One sample of a closed-form rollout (the sequential loop's per-step checks,
@@ -505,7 +525,7 @@ KP_DEV bool check_sample(const KpProblem& P, const Env& E, const float* xs, floa
 // interleaved, and contiguous runs per thread were all slower: the shorter a
 // chunk, the less the lanes of a warp wait on each other's chunk tails).
 template <int MODEL>
-KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, unsigned char* dyn) {
+KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, unsigned char* dyn, const PropCtl& pc) {
     constexpr int N = Model<MODEL>::N;
     constexpr int M = Model<MODEL>::M;
     constexpr uint32_t T = PropCfg<MODEL>::T;
@@ -526,9 +546,8 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
     uint32_t* const len_lo = reinterpret_cast<uint32_t*>(dyn + P.flat_len);  // [FB]
     uint32_t* const len_hi = len_lo + FB;                                   // [FB]
     KpCtl* ctl = B.ctl;
-    const uint32_t done = ctl->done, n_items = ctl->n_items, it = ctl->iter;
-    const unsigned long long seed = ctl->seed;
-    if (done) return;
+    const uint32_t n_items = pc.n_items, it = pc.it;
+    const unsigned long long seed = pc.seed;
     if (threadIdx.x < 6) fcnt[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_prop_ns = globaltimer();
     const uint32_t CH = min(T * PropCfg<MODEL>::MAXG, ((n_items + gridDim.x - 1) / gridDim.x + 31u) & ~31u);
@@ -757,7 +776,7 @@ KP_DEV void flat_phase(const KpProblem& P, const KpBuffers& B, const Env& E, uns
         __syncthreads();
     }
     KP_STAMP_MAX(it, 18);  // diagnostic build: admissions issued (latest block)
-    count_flush(ctl, c, fcnt, lane);
+    count_flush(ctl, c, fcnt, lane, it);
 }
 
 template <int MODEL>
@@ -774,17 +793,45 @@ __global__ void __launch_bounds__(PropCfg<MODEL>::T, PropCfg<MODEL>::MIN_BLOCKS)
     KP_STAMP_B0(it_s, 14, globaltimer());
 #endif
     unsigned char* const dyn = reinterpret_cast<unsigned char*>(kp_env_smem);
+    // Control block (one round trip).  First, the previous boundary's
+    // best-solution bookkeeping and stop-at-first-solution (they need every
+    // goal commit of the scatter, complete now): block 0 records, every
+    // block takes the same stop decision from the same `best`.
+    const PropCtl pc = load_prop_ctl(B.ctl);
+    const bool stop = !pc.done && pc.stop_first && pc.best != ~0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        KpCtl* ctl = B.ctl;
+        ctl->cur_iter = pc.it;
+        if (pc.done) {
+            // stopped at an earlier boundary: that grid has completed, so the
+            // control block and the store are final — tell the host
+            __threadfence_system();
+            *B.host_done = pc.seq;  // (a no-op launch of an earlier solve writes that solve's number)
+        } else {
+            if (pc.best < pc.tl_best) goal_bookkeeping(*ctl);
+            if (stop) {
+                ctl->done_iter = pc.it;
+                ctl->done = 1;
+                __threadfence_system();
+                *B.host_done = pc.seq;
+            }
+        }
+    }
+    if (pc.done || stop) {
+        env_wait();  // no block exits with its bulk copy in flight
+        return;
+    }
     if constexpr (closed_form<MODEL>()) {
         // small launches are latency-bound: flatten them into samples; large
         // ones are issue-bound, where the step-sorted path runs fewer instructions
-        if (P.flat_on && B.ctl->n_items <= P.flat_max) {
-            flat_phase<MODEL>(P, B, E, dyn);
+        if (P.flat_on && pc.n_items <= P.flat_max) {
+            flat_phase<MODEL>(P, B, E, dyn, pc);
             env_wait();  // no block exits with its bulk copy in flight
             KP_STAMP_MAX(it_s, 2);
             return;
         }
     }
-    propagate_phase<MODEL>(P, B, *reinterpret_cast<PropSmem<MODEL>*>(dyn + P.seq_base), E);
+    propagate_phase<MODEL>(P, B, *reinterpret_cast<PropSmem<MODEL>*>(dyn + P.seq_base), E, pc);
     env_wait();
     KP_STAMP_MAX(it_s, 2);
 }
@@ -981,7 +1028,7 @@ KP_DEV void select_reduce_phase(const KpProblem& P, const KpBuffers& B) {
         si_b = B.live_si[1][e0];
     }
     const uint32_t done = ctl->done, it = ctl->iter, n_live = ctl->n_live, n_items = ctl->n_items;
-    const uint32_t n_adm = ctl->n_adm_iter;
+    const uint32_t n_adm = ctl->n_adm_p[it & 1];
     if (done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_sel_ns = globaltimer();
     __shared__ uint32_t s_st[7];
@@ -1126,56 +1173,48 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS, (SPEC ? 5 : 8) * 256 / KP_S
     KP_STAMP_MAX(it_s, 6);
 }
 
-// Close an iteration: counts, stats, best / timeline / TTFS
-// from %globaltimer, trace record, termination.  One thread of the last block.
-// The control-block fields the boundary reads, all written before the
-// scatter kernel starts (by the previous boundary, k_start, propagate and
-// select_reduce) except `best`, which goal commits lower during the scatter.
-// Every scatter block's thread 0 loads them beside its own control-block
-// reads (the same round trip) and parks them in shared memory, so the closing
-// block needs no further round trip unless a goal node was committed.
+// Close an iteration: counts, stats, trace record,
+// termination.  Written by select_scatter's block 0 (thread 0) as soon as the
+// tile prefix gives it the totals, while the other blocks still write their
+// tiles: it reads nothing they write, and they read the iteration's parity
+// view of the control block, not the fields it overwrites (kp_types.h).  The
+// best-solution bookkeeping — which needs every goal commit — is the next
+// propagate's first step (goal_bookkeeping), and stop-at-first-solution ends
+// the solve there.  Its inputs were written before the scatter started (by
+// the previous boundary, k_start, propagate and select_reduce); block 0's
+// thread 0 loads them beside its control-block reads.
 struct BoundaryIn {
-    unsigned long long best, tl_best, t_start, first_ns, deadline, t_prop, t_sel;
+    unsigned long long t_start, deadline, t_prop, t_sel;
     unsigned long long st_att, st_com, st_drop;
-    uint32_t tl_len, max_iter_abs, stop_first, n_valid;
+    uint32_t max_iter_abs, n_valid;
 };
 
 KP_DEV BoundaryIn load_boundary_in(const KpCtl* ctl) {
     BoundaryIn b;
-    b.best = ctl->best;
-    b.tl_best = ctl->tl_best;  // == timeline_len ? timeline[timeline_len - 1].best : ~0
     b.t_start = ctl->t_start_ns;
-    b.first_ns = ctl->first_ns;
     b.deadline = ctl->deadline_ns;
     b.t_prop = ctl->t_prop_ns;
     b.t_sel = ctl->t_sel_ns;
     b.st_att = ctl->stats.attempted;
     b.st_com = ctl->stats.committed;
     b.st_drop = ctl->stats.dropped_capacity;
-    b.tl_len = ctl->timeline_len;
     b.max_iter_abs = ctl->max_iter_abs;
-    b.stop_first = ctl->stop_first;
     b.n_valid = ctl->n_valid_iter;
     return b;
 }
 
-// bin: the prefetched inputs; best: the current best (re-read by the caller
-// when a goal node was committed this iteration); t_scat: the closing
-// block's entry stamp.
+// bin: the prefetched inputs; t_scat: block 0's entry stamp.
 KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t it, uint32_t n_items,
                                uint32_t tot_keep, uint32_t tot_va, uint32_t tot_commit, uint32_t n_nodes,
-                               uint32_t accepted, const BoundaryIn& bin, unsigned long long best,
-                               unsigned long long t_scat) {
+                               uint32_t accepted, const BoundaryIn& bin, unsigned long long t_scat) {
     KpCtl* ctl = B.ctl;
     const uint32_t S = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
     const unsigned long long now = globaltimer();
     const uint32_t it1 = it + 1;
-    const uint32_t tl_len = bin.tl_len;
-    const unsigned long long prev = bin.tl_best;
-    const unsigned long long t_start = bin.t_start, first_ns = bin.first_ns, deadline = bin.deadline;
+    const unsigned long long t_start = bin.t_start, deadline = bin.deadline;
     const unsigned long long t_prop = bin.t_prop, t_sel = bin.t_sel;
-    const uint32_t max_iter_abs = bin.max_iter_abs, stop_first = bin.stop_first;
+    const uint32_t max_iter_abs = bin.max_iter_abs;
     const unsigned long long st_att = bin.st_att, st_com = bin.st_com;
     const unsigned long long st_drop = bin.st_drop;
     const uint32_t n_valid = bin.n_valid;
@@ -1193,22 +1232,6 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
     ctl->n_va = n_va1;
     ctl->iter = it1;
     ctl->t_last_ns = now;
-    if (best < prev) {  // strict improvement at this iteration boundary (cost bits are the high word)
-        if (tl_len < KP_TIMELINE_CAP) {
-            KpTimeline& t = ctl->timeline[tl_len];
-            t.iteration = it1;
-            t.t_ns = now - t_start;
-            t.best = best;
-            ctl->timeline_len = tl_len + 1;
-            ctl->tl_best = best;
-        }
-        if (first_ns == 0) {
-            ctl->first_ns = now - t_start;
-            ctl->first_iter = it1;
-        }
-        ctl->best_ns = now - t_start;
-        ctl->best_iter = it1;
-    }
     {
         KpTraceRec& tr = B.trace[it % KP_TRACE_CAP];
         tr.t_ns = now - t_start;
@@ -1224,45 +1247,47 @@ KP_DEV void iteration_boundary(const KpProblem& P, const KpBuffers& B, uint32_t 
         tr.t_scat = static_cast<uint32_t>(t_scat - t_start);
     }
     bool done = false;
+    uint32_t items1 = static_cast<uint32_t>(items);
     if (items > S) {
         ctl->error = 8;  // KP_ERR_SLOT_OVERFLOW
         done = true;
-        ctl->n_items = 0;
-    } else {
-        ctl->n_items = static_cast<uint32_t>(items);
+        items1 = 0;
     }
+    ctl->n_items = items1;
+    // the next iteration's view for its select_scatter blocks
+    ctl->view_live[it1 & 1] = n_live1;
+    ctl->view_items[it1 & 1] = items1;
+    ctl->view_nodes[it1 & 1] = n_nodes1;
+    ctl->n_adm_p[it1 & 1] = 0;
     if (max_iter_abs && it1 >= max_iter_abs) done = true;
     if (deadline && now >= deadline) done = true;
-    if (stop_first && best != ~0ull) done = true;
     if (n_live1 == 0) done = true;
-    ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
-    ctl->n_adm_iter = 0;
     ctl->n_valid_iter = 0;
     // split the next propagate's rollouts when many items stop early (invalid):
     // the compaction then pays for its second pass (scripts/split_sim.py)
     ctl->split = (n_items - min(n_valid, n_items)) * 4u >= n_items && n_items > 0 ? 1u : 0u;
-    if (done) {
+    if (done) {  // the host learns it from the next propagate (this grid may still be writing)
+        ctl->done_iter = it1;
         ctl->done = 1;
-        __threadfence_system();
-        *B.host_done = 1;
     }
 }
 
 KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     KpCtl* ctl = B.ctl;
-    // every control-block read up front: one round trip
-    const uint32_t done = ctl->done, it = ctl->iter, n_live = ctl->n_live, n_items = ctl->n_items;
-    const uint32_t n_adm = ctl->n_adm_iter, n_nodes = ctl->n_nodes;
-    __shared__ unsigned int s_last, s_goal;
+    // every control-block read up front: one round trip.  Block 0 writes the
+    // boundary while the other blocks run, so they read this iteration's view
+    // (parity of cur_iter, written by propagate), not the fields it overwrites.
+    const uint32_t it = ctl->cur_iter, done_iter = ctl->done_iter;
+    const uint32_t n_live = ctl->view_live[it & 1], n_items = ctl->view_items[it & 1];
+    const uint32_t n_nodes = ctl->view_nodes[it & 1], n_adm = ctl->n_adm_p[it & 1];
     __shared__ BoundaryIn s_bin;
     __shared__ unsigned long long s_t0;
-    if (threadIdx.x == 0) {  // the boundary's inputs, in the same round trip as the fields above
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // the boundary's inputs, in the same round trip
         s_bin = load_boundary_in(ctl);
-        s_goal = 0;
         s_t0 = globaltimer();
     }
-    if (done) return;
+    if (done_iter <= it) return;  // the solve stopped before this iteration
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_scat_ns = globaltimer();
     __shared__ uint32_t s_red[6][KP_SELECT_THREADS / 32];
     const SelLayout ly = sel_layout(n_live, n_items, n_adm);  // as select_reduce
@@ -1348,6 +1373,18 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     KP_STAMP_MAX(it, 15);  // diagnostic build: prefix pass done (latest block)
     const uint32_t remaining = P.capacity - n_nodes;
     const uint32_t accepted = tot_commit < remaining ? tot_commit : remaining;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // the iteration boundary, right away: nothing it reads comes from the
+        // other blocks (their node-store and list writes are read by later
+        // kernels, after this grid completes)
+#ifdef KP_STAMPS
+        kp_stamps[it & 63][10] = globaltimer();
+#endif
+        iteration_boundary(P, B, it, n_items, tot_keep, tot_va, tot_commit, n_nodes, accepted, s_bin, s_t0);
+#ifdef KP_STAMPS
+        kp_stamps[it & 63][12] = globaltimer();
+#endif
+    }
     Cnt3 run{acc[0], acc[1], acc[2]};
     const uint32_t cap = P.capacity, S = P.max_slots;
     const uint32_t lam = static_cast<uint32_t>(P.lambda);
@@ -1391,10 +1428,8 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
         live_n[tot_keep + rank] = make_uint4(id, reg, abits, par);
         live_si_n[tot_keep + rank] = KP_ST_ACTIVE;
         va_n[tot_va + rank] = id;
-        if (goal) {  // Alg. 4 lines 5-7
+        if (goal)  // Alg. 4 lines 5-7 (bookkept by the next propagate)
             atomicMin(&ctl->best, (static_cast<unsigned long long>(abits) << 32) | id);
-            s_goal = 1u;
-        }
     };
     for (uint32_t tile = tb; tile < te; ++tile) {
         const Elem el = tile == tb ? first : load_elem(tile);
@@ -1438,46 +1473,7 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
             }
         }
     }
-    // the last block to take a ticket closes the iteration (below)
     KP_STAMP_MAX(it, 4);  // diagnostic build: writes issued (latest block)
-    // The ticket also carries, from bit 20 up, the number of blocks that
-    // committed a goal node: without one, `best` is still the prefetched value.
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned int prev;
-        const unsigned int add = 1u + (s_goal ? (1u << 20) : 0u);
-#ifdef KP_STAMPS
-        const unsigned long long t_pre = globaltimer();
-        atomicMax(&kp_stamps[it & 63][13], t_pre);
-#endif
-        // Of the blocks' writes only the goal commits (atomicMin on best) are
-        // read by the closing block; the lists and the node store are read by
-        // later kernels (grid completion orders them), and every block's
-        // control-block reads are complete (their values were used).  So a
-        // block without a goal commit takes its ticket relaxed (no wait for
-        // its stores to drain: forest +1.3 %), a goal block with release
-        // semantics, and the closing block acquires (fence after its ticket)
-        // when some block committed a goal node.
-        if (s_goal)
-            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(prev) : "l"(&ctl->ticket_b), "r"(add) : "memory");
-        else
-            asm volatile("atom.add.relaxed.gpu.u32 %0, [%1], %2;" : "=r"(prev) : "l"(&ctl->ticket_b), "r"(add) : "memory");
-        s_last = (prev & 0xFFFFFu) == n_part - 1;
-        if (s_last) {
-            if ((prev >> 20) != 0u) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the goal blocks' best
-#ifdef KP_STAMPS
-            kp_stamps[it & 63][10] = t_pre;
-            kp_stamps[it & 63][11] = globaltimer();
-#endif
-            const bool any_goal = s_goal || (prev >> 20) != 0u;
-            const unsigned long long best = any_goal ? *reinterpret_cast<volatile unsigned long long*>(&ctl->best)
-                                                     : s_bin.best;
-            iteration_boundary(P, B, it, n_items, tot_keep, tot_va, tot_commit, n_nodes, accepted, s_bin, best, s_t0);
-#ifdef KP_STAMPS
-            kp_stamps[it & 63][12] = globaltimer();
-#endif
-        }
-    }
 }
 
 // 3 blocks/SM (up to 80 registers): at 4 (64 registers) the committed
@@ -1536,7 +1532,8 @@ __global__ void k_reset_root(KpProblem P, KpBuffers B, unsigned long long seed) 
 }
 
 // Start of a kp_solve call: budget, iteration cap, immediate termination test.
-__global__ void k_start(KpBuffers B, unsigned long long budget_ns, uint32_t max_iters, uint32_t stop_first) {
+__global__ void k_start(KpBuffers B, unsigned long long budget_ns, uint32_t max_iters, uint32_t stop_first,
+                        uint32_t seq) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     KpCtl* ctl = B.ctl;
     const unsigned long long now = globaltimer();
@@ -1544,13 +1541,18 @@ __global__ void k_start(KpBuffers B, unsigned long long budget_ns, uint32_t max_
     ctl->deadline_ns = budget_ns ? now + budget_ns : 0ull;
     ctl->max_iter_abs = max_iters ? ctl->iter + max_iters : 0u;
     ctl->stop_first = stop_first;
-    ctl->ticket_b = 0;
     ctl->prop_cursor = 0;
-    ctl->n_adm_iter = 0;
+    const uint32_t it = ctl->iter;
+    ctl->n_adm_p[it & 1] = 0;
+    ctl->view_live[it & 1] = ctl->n_live;  // this iteration's view for select_scatter
+    ctl->view_items[it & 1] = ctl->n_items;
+    ctl->view_nodes[it & 1] = ctl->n_nodes;
     bool done = ctl->error != 0 || ctl->n_live == 0 || (stop_first && ctl->best != ~0ull);
+    ctl->done_iter = done ? it : 0xFFFFFFFFu;
     ctl->done = done ? 1u : 0u;
     __threadfence_system();
-    *B.host_done = done ? 1u : 0u;
+    ctl->solve_seq = seq;
+    *B.host_done = done ? seq : 0u;
     __threadfence_system();
 }
 
@@ -1817,8 +1819,8 @@ cudaError_t launch_reset(const KpProblem& P, const KpBuffers& B, unsigned long l
 }
 
 cudaError_t launch_start(const KpBuffers& B, unsigned long long budget_ns, uint32_t max_iters, uint32_t stop_first,
-                         cudaStream_t st) {
-    k_start<<<1, 32, 0, st>>>(B, budget_ns, max_iters, stop_first);
+                         uint32_t seq, cudaStream_t st) {
+    k_start<<<1, 32, 0, st>>>(B, budget_ns, max_iters, stop_first, seq);
     return cudaGetLastError();
 }
 
@@ -1857,7 +1859,7 @@ __global__ void k_sweep_prepare(KpProblem P, KpBuffers B, uint32_t n) {
         c->n_nodes = n;
         c->n_items = n * static_cast<uint32_t>(P.lambda);
         c->prop_cursor = 0;
-        c->n_adm_iter = 0;
+        c->n_adm_p[0] = 0;
         c->n_valid_iter = 0;
         c->split = 0;  // no previous iteration to measure the invalid share on
         c->stats = KpStats{};

@@ -104,6 +104,15 @@ struct KpStats {
     unsigned long long live_scanned, ancestor_hops, slots_scanned, admitted_checked;
 };
 
+#ifdef __CUDACC__
+#define KP_HD __host__ __device__
+#else
+#define KP_HD
+#endif
+
+struct KpCtl;
+KP_HD inline void goal_bookkeeping(KpCtl& c);
+
 struct KpTimeline {
     unsigned long long iteration;
     unsigned long long t_ns;
@@ -130,12 +139,22 @@ struct KpCtl {
     // produced by select_reduce for select_scatter
     uint32_t n_tiles;
     uint32_t tot_keep, tot_va, tot_commit, accepted;
-    uint32_t ticket_b;        // scatter blocks done (the last one closes the iteration)
+    uint32_t ticket_b;        // (unused since the early boundary)
     uint32_t prop_cursor;     // dynamic chunk cursor of k_propagate (reset at every boundary)
     uint32_t n_adm_iter;      // slots admitted by this iteration's propagate (reset at every boundary);
                               // selects the select kernels' element layout (per slot / per mask word)
     uint32_t n_valid_iter;    // valid rollouts of this iteration's propagate (reset at every boundary)
     uint32_t split;           // 1: the next propagate splits its rollouts (>= 1/4 of the last iteration's were invalid)
+    // The iteration boundary is written by select_scatter's block 0 as soon as
+    // it has the totals, while the other blocks may still read the control
+    // block: they read this iteration's view (parity = iteration & 1), which
+    // the boundary writes for the next one, and the iteration number from
+    // cur_iter (written by propagate).  done_iter: the iteration count at
+    // which `done` was raised (a scatter skips only iterations after it).
+    uint32_t cur_iter, done_iter;
+    uint32_t solve_seq;       // kp_solve call number: the value the device writes to the host's done word
+    uint32_t n_adm_p[2];      // slots admitted by propagate, per iteration parity (cleared by the previous boundary)
+    uint32_t view_live[2], view_items[2], view_nodes[2];
     // run bookkeeping
     uint32_t max_iter_abs;    // stop when iter >= this (0 = unlimited)
     uint32_t stop_first;
@@ -150,6 +169,34 @@ struct KpCtl {
     KpStats stats;
     KpTimeline timeline[KP_TIMELINE_CAP];
 };
+
+// Best-solution bookkeeping of the last iteration boundary (SPEC.md:362-367,
+// :440): a strict improvement of `best` over the last timeline entry appends
+// an entry stamped with that boundary's time and iteration count, and sets
+// the first / latest solution time.  Run by the next propagate (block 0,
+// before anything else) and, for the last boundary of a solve, on the host
+// copy of the control block (fetch_ctl): the same result either way.
+KP_HD inline void goal_bookkeeping(KpCtl& c) {
+    const unsigned long long best = c.best;
+    if (!(best < c.tl_best)) return;
+    const unsigned long long t = c.t_last_ns - c.t_start_ns;
+    const uint32_t it = c.iter;
+    if (c.timeline_len < KP_TIMELINE_CAP) {
+        KpTimeline& e = c.timeline[c.timeline_len];
+        e.iteration = it;
+        e.t_ns = t;
+        e.best = best;
+        c.timeline_len += 1;
+        c.tl_best = best;
+    }
+    if (c.first_ns == 0) {
+        c.first_ns = t;
+        c.first_iter = it;
+    }
+    c.best_ns = t;
+    c.best_iter = it;
+}
+
 
 // Device buffer set of one planner.
 struct KpBuffers {
@@ -189,5 +236,5 @@ struct KpBuffers {
     KpTraceRec* trace;      // [KP_TRACE_CAP] ring, one record per iteration boundary
     float* x0;              // [KP_MAX_N] current query's start state (H2D per query)
     KpCtl* ctl;
-    volatile uint32_t* host_done;  // mapped pinned word (device writes 1 at termination)
+    volatile uint32_t* host_done;  // mapped pinned word (device writes the solve's sequence number at termination)
 };
