@@ -712,6 +712,7 @@ int kp_create(const kp_problem_desc* problem, const kp_config_desc* config, int 
         cuda_check(cudaHostAlloc(&hc, sizeof(KpCtl), cudaHostAllocDefault), "cudaHostAlloc ctl");
         pl->h_ctl = static_cast<KpCtl*>(hc);
         pl->P.sel_spec = 1;
+        if (const char* v = std::getenv("KP_SEL_SPEC")) pl->P.sel_spec = std::atoi(v) ? 1 : 0;  // A/B hook
         kp::plan_propagate_smem(pl->P);
         cuda_check(kp::set_propagate_smem(P), "smem attribute");
         const int occ = std::max(1, kp::propagate_occupancy(P));
