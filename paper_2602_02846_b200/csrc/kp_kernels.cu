@@ -31,14 +31,16 @@
 //                        ids count + rank in slot order (so ids equal the
 //                        reference's workers=1 serial order), their records
 //                        are written to the SoA node store, goal leaves do a
-//                        64-bit atomicMin on (cost bits << 32 | id).  The last
-//                        block closes the iteration: counts, stats, best /
-//                        timeline / TTFS from %globaltimer, termination (its
-//                        inputs prefetched with the block's control-block reads).
+//                        64-bit atomicMin on (cost bits << 32 | id).  Block 0
+//                        closes the iteration as soon as its tile prefix gives
+//                        it the totals: counts, stats, termination (the other
+//                        blocks read a per-parity view of the control block);
+//                        the best / timeline / TTFS bookkeeping, which needs
+//                        every goal commit, is the next propagate's first step.
 //
-// No kernel waits on another block: cross-block results flow through the
-// "last block" ticket pattern (an atomic counter), never a spin; the one
-// in-block wait is the split rollouts' second pass behind a block barrier.
+// No kernel waits on another block: cross-block results flow through kernel
+// boundaries (PDL), never a spin; the one in-block wait is the split
+// rollouts' second pass behind a block barrier.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cmath>
@@ -65,7 +67,7 @@ KP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::
 // Diagnostic build only (-DKP_STAMPS, scripts/stamps.py): %globaltimer stamps
 // of kernel phases per iteration (a ring of 64 iterations x 32 points) — block
 // 0's entry / PDL release / control-block arrival and the latest block exit
-// of each kernel, the closing scatter block's ticket and boundary.
+// of each kernel, the scatter's iteration boundary.
 #ifdef KP_STAMPS
 __device__ unsigned long long kp_stamps[64][32];
 #define KP_STAMP_B0(it, k, t)                                                        \
