@@ -1856,6 +1856,7 @@ __global__ void k_sweep_prepare(KpProblem P, KpBuffers B, uint32_t n) {
     if (i == 0) {
         KpCtl* c = B.ctl;
         c->done = 0;
+        c->stop_first = 0;  // propagate's stop-at-first-solution test must not end a sweep launch
         c->iter = 0;
         c->n_va = n;
         c->n_nodes = n;
