@@ -88,3 +88,29 @@ def test_batch_engine_matches_single_planner():
             for k in ("best_cost", "best_leaf", "node_count", "propagations_attempted", "propagations_valid",
                       "iterations", "nodes_pruned_terminal"):
                 assert r[k] == one[k], (sd, k, r[k], one[k])
+
+
+def test_stop_at_first_solution_then_sweep_and_replay():
+    """Stop-at-first-solution ends the solve at the first iteration boundary
+    with a solution (the next propagate takes that decision, after the
+    boundary's goal commits); the same seed run for exactly that many
+    iterations reproduces it, and the planner still sweeps afterwards (the
+    stop test must not end a sweep launch)."""
+    s = scenarios.load("forest_di6", capacity=1 << 18, max_slots=1 << 21)
+    with Planner(s, seed=3) as g:
+        g.set_stop_at_first_solution(True)
+        a = g.solve(5.0, 0)
+        assert a["found"] and a["iterations"] == a["first_solution_iteration"]
+        tl_a = g.timeline()
+        assert len(tl_a) == 1 and tl_a[0]["iteration"] == a["iterations"]
+        g.set_stop_at_first_solution(False)
+        g.reset(3)
+        b = g.solve(0.0, a["iterations"])
+        assert b["best_cost"] == a["best_cost"] and b["best_leaf"] == a["best_leaf"]
+        assert b["node_count"] == a["node_count"] and b["first_solution_iteration"] == a["iterations"]
+        assert [(e["iteration"], e["cost"], e["leaf"]) for e in g.timeline()] == [(e["iteration"], e["cost"], e["leaf"]) for e in tl_a]
+        g.set_stop_at_first_solution(True)
+        g.reset(3)
+        g.solve(5.0, 0)
+        ms, prof = g.sweep(1024, launches=1)
+        assert prof["items"] == 1024 * s["planner"]["lambda"] and prof["rk4_steps"] > prof["items"]
