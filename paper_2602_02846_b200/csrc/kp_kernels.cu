@@ -888,6 +888,12 @@ KP_DEV uint32_t prune_node(const KpProblem& P, const KpBuffers& B, uint4 rec, ui
     const uint32_t st = si & 0xFFu;
     KP_ASSERT(rec.y < P.n_regions, 21);
     KP_ASSERT(st != KP_ST_TERMINAL, 22);  // Terminal nodes never stay in the live list
+    // an Active node's parent link is loaded beside its own region cost (the
+    // ancestor walk's first hop no longer waits for rule 1's round trip)
+    const int32_t p = static_cast<int32_t>(rec.w);
+    const bool walks = st == KP_ST_ACTIVE && P.deact == 0 && p >= 0;
+    uint4 L = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+    if (walks) L = B.link[p];  // {parent, region, acc, -}
     if (rec.z > B.rc[rec.y]) {  // (1) dominated -> Terminal (absorbing)
         B.status[g] = KP_ST_TERMINAL;
         ++*term;
@@ -909,9 +915,7 @@ KP_DEV uint32_t prune_node(const KpProblem& P, const KpBuffers& B, uint4 rec, ui
     // is issued together with this hop's region-cost load, so the chain costs
     // about one L2 round trip per hop.
     bool dominated = P.deact != 0;
-    const int32_t p = static_cast<int32_t>(rec.w);
-    if (!dominated && p >= 0) {
-        uint4 L = B.link[p];  // {parent, region, acc, -}
+    if (walks) {
         for (;;) {
             ++*hops;
             const int32_t q = static_cast<int32_t>(L.x);
