@@ -459,11 +459,26 @@ def other_configs(args, budget):
                     r = g.solve(b)
                     res.append(r)
                     dev += r["elapsed_s"]
+                # time to first solution over seeds 0..N-1 (stop-at-first queries)
+                dist = None
+                if args.dist_seeds > 0:
+                    g.set_stop_at_first_solution(True)
+                    tt_d = []
+                    for sd in range(args.dist_seeds):
+                        g.reset(sd)
+                        r = g.solve(max(b, 1.0))
+                        if r["found"]:
+                            tt_d.append(r["first_solution_s"] * 1e3)
+                    g.set_stop_at_first_solution(False)
+                    dist = {"seeds": [0, args.dist_seeds - 1], "ms_to_first_solution_median": _median(tt_d),
+                            "ms_to_first_solution_p25_p75": _quart(tt_d),
+                            "success_rate": len(tt_d) / args.dist_seeds, "budget_s": max(b, 1.0)}
             tt = [r["first_solution_s"] * 1e3 for r in res if r["found"]]
             out[cfg] = {"budget_ms": b * 1e3, "queries": len(res), "success_rate": len(tt) / len(res),
                         "ms_to_first_solution_median": _median(tt),
                         "solution_cost_at_budget_median": _median([r["best_cost"] for r in res if r["found"]]),
-                        "node_propagations_per_sec": sum(r["propagations_attempted"] for r in res) / dev}
+                        "node_propagations_per_sec": sum(r["propagations_attempted"] for r in res) / dev,
+                        "over_seeds": dist}
         except Exception as e:  # noqa: BLE001
             out[cfg] = {"error": str(e)[:200]}
     try:
