@@ -588,6 +588,9 @@ def roofline(scenario, pa, pb):
         "issue": issue,
         "peak_src": pk["fp32_src"],
         "ops_per_launch": ops_launch, "avg_launch_us": t_prop * 1e6, "launches": n_prop,
+        # propagations per second of the propagate kernel alone (SURVEY.md §8d:
+        # reported beside the whole-query rate; per-launch CUDA events, serialised)
+        "items_per_s_kernel_only": d["items"] / d["t_propagate_s"] if d["t_propagate_s"] > 0 else None,
         "ops_convention": "FP32 lane-ops of the pinned recipe: FFMA, FADD, FMUL, FSETP, FMNMX, FDIV each = 1",
         "share_of_iteration_time": d["t_propagate_s"] / t_total if t_total else None,
         "select": {"kernel": "k_select_reduce", "bound": "latency (L2-resident dependent loads; HBM shown for scale)",
