@@ -1402,7 +1402,8 @@ KP_DEV void scatter_phase(const KpProblem& P, const KpBuffers& B) {
     // one committed slot -> node id n_nodes + rank (slot order), store, lists, best
     auto commit_node = [&](uint32_t sl, uint32_t rank, bool goal) {
         const uint32_t id = n_nodes + rank;
-        KP_ASSERT(id < cap && sl < S && sl / lam < ctl->n_va, 30);
+        // (this iteration's frontier: n_items / lambda; ctl->n_va may already be the next one's)
+        KP_ASSERT(id < cap && sl < S && sl < n_items, 30);
         KP_ASSERT(tot_keep + rank < cap && tot_va + rank < cap, 31);
         // every load of the slot record first, then the stores: interleaved,
         // the possible aliasing of the float arrays kept each load behind the
