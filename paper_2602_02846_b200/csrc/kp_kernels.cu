@@ -1494,7 +1494,7 @@ __global__ void __launch_bounds__(KP_SELECT_THREADS, KP_SCATTER_MINB) k_select_s
     KP_T1;
     pdl_trigger();
 #ifdef KP_STAMPS
-    const uint32_t it_s = B.ctl->iter;
+    const uint32_t it_s = B.ctl->cur_iter;  // ctl->iter may already be the next iteration's (early boundary)
     KP_STAMP_B0(it_s, 7, kp_t_entry);
     KP_STAMP_B0(it_s, 8, kp_t_pdl);
     KP_STAMP_B0(it_s, 9, globaltimer());
