@@ -1,5 +1,8 @@
 """Per-iteration device trace of one query (graph mode, no profiler): time per
-iteration split into propagate / select_reduce / select_scatter / gaps."""
+iteration split into propagate / select_reduce / select_scatter / gaps.
+Since the early iteration boundary (select_scatter's block 0 writes it right
+after its tile prefix), `scat` is block 0's entry -> boundary and the `gap`
+after it includes the rest of the scatter's tile writes."""
 import sys
 import numpy as np
 sys.path.insert(0, '.')
